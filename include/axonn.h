@@ -1,0 +1,251 @@
+/*
+ * axonn.h — C ABI of libaxonn.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of AxoNN's 4D hybrid parallelism (arXiv 2502.08145):
+ * the 3D parallel matrix multiply (3D PMM) of one transformer FC layer on a
+ * Gx x Gy x Gz grid nested in Gd-way data parallelism.
+ *
+ * Citations "PAPER.md:N" are lines of the paper's LaTeX source; "Alg. 1" is
+ * Algorithm 1.  DESIGN.md lists every reading (R1..R16)
+ * taken where the paper is silent or ambiguous.
+ *
+ * Conventions for every call
+ *   - Return value: AXONN_OK or an error status.  A thread-local message is
+ *     available from axonn_last_error() until the next failing call.
+ *   - Device pointers are caller-owned CUDA memory on the calling rank's
+ *     device (cudaMalloc/torch allocations).  Host pointers are marked "host".
+ *   - Device-side calls are stream-ordered on the `stream` argument (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream): they
+ *     enqueue work and return without synchronising.  Asynchronous CUDA /
+ *     NCCL failures surface as AXONN_ERR_CUDA / AXONN_ERR_NCCL on a later call.
+ *   - All matrices are row-major with an explicit leading dimension in
+ *     elements; bf16 buffers hold IEEE bfloat16, f32 buffers IEEE binary32.
+ *   - No call ever falls back to a CPU path: if the CUDA device or the
+ *     sm_100a kernels are unavailable the call fails with AXONN_ERR_CUDA.
+ */
+#ifndef AXONN_H
+#define AXONN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AXONN_OK = 0,
+  AXONN_ERR_ARG = 1,          /* NULL pointer, negative size, bad enum           */
+  AXONN_ERR_CONFIG = 2,       /* grid factor product != world size, zero factor  */
+  AXONN_ERR_SHAPE = 3,        /* divisibility failure; message names the axis    */
+  AXONN_ERR_STATE = 4,        /* e.g. backward before forward, no grid           */
+  AXONN_ERR_INFEASIBLE = 5,   /* grid_select found no configuration              */
+  AXONN_ERR_CUDA = 6,         /* CUDA runtime/driver failure or no sm_100 device */
+  AXONN_ERR_NCCL = 7,         /* NCCL failure (sync or async)                    */
+  AXONN_ERR_UNSUPPORTED = 8   /* valid request this build does not implement    */
+} axonn_status_t;
+
+typedef enum {
+  AXONN_BF16 = 0,             /* bf16 storage, fp32 accumulate on tcgen05 */
+  AXONN_F32 = 1               /* fp32 storage and SIMT fp32 arithmetic: test mode            */
+} axonn_dtype_t;
+
+/* Message of the last failing call on this thread ("" if none). Never NULL. */
+const char* axonn_last_error(void);
+/* ABI version, major*100 + minor. */
+int axonn_version(void);
+
+/* ======================================================================== */
+/* Process bootstrap (one process per GPU).                                  */
+/* ======================================================================== */
+
+/* Fill `id` (host, 128 bytes) with a fresh NCCL unique id.  Call on world
+ * rank 0 only; the caller broadcasts the bytes to every rank out of band
+ * (torch.distributed).  Errors: AXONN_ERR_NCCL. */
+axonn_status_t axonn_unique_id(unsigned char id[128]);
+
+/* Bind this process to `cuda_device` and create the world communicator
+ * (world_size ranks).  world_size == 1 creates no communicator and needs no
+ * id (id may be NULL).  Errors: ARG, CUDA, NCCL; STATE if already bootstrapped. */
+axonn_status_t axonn_bootstrap(int world_rank, int world_size, const unsigned char* id,
+                               int cuda_device);
+
+/* ======================================================================== */
+/* The 4D virtual grid.                 */
+/*   rank r <-> (i, j, k, d),  r = i + Gx*(j + Gy*(k + Gz*d))               */
+/*   X innermost, then Y, then Z, data-parallel outermost */
+/* ======================================================================== */
+
+/* Create the four axis sub-communicators X, Y, Z, DATA (members ordered by
+ * the axis coordinate) and this rank's streams.  Requires bootstrap.
+ * Errors: CONFIG (gx*gy*gz*gd != world size, or a factor < 1), STATE, NCCL. */
+axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd);
+/* This rank's coordinates (host out-pointers). Errors: STATE (no grid). */
+axonn_status_t axonn_grid_coords(int* i, int* j, int* k, int* d);
+/* Destroy communicators, streams and every outstanding layer handle's
+ * communication state.  Safe to call twice. */
+axonn_status_t axonn_grid_finalize(void);
+
+/* Pure host helpers (no device, no communicator): the rank <-> coordinate
+ * bijection and the members of rank's group along `axis` (0=X,1=Y,2=Z,3=DATA),
+ * written to `members` (host, capacity >= extent of that axis) in coordinate
+ * order.  Errors: CONFIG, ARG. */
+axonn_status_t axonn_rank_to_coords(int rank, int gx, int gy, int gz, int gd, int coords[4]);
+axonn_status_t axonn_group_members(int rank, int gx, int gy, int gz, int gd, int axis,
+                                   int* members);
+
+/* ======================================================================== */
+/* One FC layer, Algorithm 1.                             */
+/* ======================================================================== */
+
+typedef struct {
+  int64_t m;          /* global tokens: rows of X over ALL data-parallel replicas */
+  int64_t k;          /* input features (rows of W)                               */
+  int64_t n;          /* output features (cols of W)                              */
+  int transposed;     /* 1: X/Y roles swapped (reading R2)       */
+  int dtype;          /* axonn_dtype_t                                            */
+  int chunks;         /* forward AR pipelining: M-chunks of the local GEMM whose
+                         all-reduce starts as each finishes (0/1 = unchunked).    */
+} axonn_fc_desc_t;
+
+/* Shard geometry of one rank (readings R1, R2, R4, R6):
+ *   I_local  = X[row0 : row0+m_l, in_col0 : in_col0+k_l]         ([m_l][k_l])
+ *   W_local  = W[in_col0 : +k_l, out_col0 : +n_l]                ([k_l][n_l])
+ *   W_hat    = flat(W_local)[what_off : what_off+what_len]       (S elements)
+ *   O_local  = O[row0 : +m_l, out_col0 : +n_l]                   ([m_l][n_l])
+ * with m_l = m/(Gz*Gd), row0 = (d*Gz + k)*m_l; normal layer: k_l = k/Gy,
+ * n_l = n/Gx, in_col0 = j*k_l, out_col0 = i*n_l; transposed layer: k_l = k/Gx,
+ * n_l = n/Gy, in_col0 = i*k_l, out_col0 = j*n_l; S = k_l*n_l/Gz,
+ * what_off = k*S. */
+typedef struct {
+  int64_t m_l, k_l, n_l, row0, in_col0, out_col0, what_off, what_len;
+} axonn_geometry_t;
+
+/* Pure host: geometry of `rank` on grid (gx,gy,gz,gd).  Errors: CONFIG, ARG,
+ * SHAPE ("k=... not divisible by Gy=..."; no padding). */
+axonn_status_t axonn_shard_geometry(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
+                                    int rank, axonn_geometry_t* out);
+
+typedef struct axonn_fc* axonn_fc_t;
+
+/* Create a layer handle on the current grid; validates divisibility and
+ * allocates the handle-owned buffers (gathered W_{j,i} when Gz>1, the dW
+ * partial when Gz>1).  Errors: ARG, STATE (no grid), SHAPE, CUDA. */
+axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out);
+/* Geometry of this rank for handle `h` (host out). */
+axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
+
+/* OAG: start the Z all-gather of W_hat for the NEXT
+ * forward now, on the communication stream, after the work already enqueued
+ * on `stream`.  Optional; axonn_fc_forward issues it itself if not prefetched. */
+axonn_status_t axonn_fc_prefetch(axonn_fc_t h, const void* W_hat, void* stream);
+
+/* Forward, Alg. 1 lines 1-7:
+ *   W_{j,i} = all-gather_z(W_hat)            (line 2; skipped when Gz == 1)
+ *   Ô       = I_local x W_{j,i}               (line 3; tcgen05 GEMM, fp32 acc)
+ *   O_local = all-reduce_y(Ô)                 (line 4; over X if transposed)
+ * I_local [m_l][k_l] (ld = k_l), W_hat [what_len], O_local [m_l][n_l]
+ * (ld = n_l), all of desc.dtype.  O_local holds Ô rounded to the dtype
+ * before the all-reduce (R8).  Line 5 caches I_local (caller keeps it alive
+ * and unmodified until backward is enqueued) and W_{j,i} (handle-owned; when
+ * Gz == 1 W_{j,i} IS W_hat, which must then also stay alive).
+ * Errors: ARG, STATE (no grid), CUDA, NCCL. */
+axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W_hat,
+                                void* O_local, void* stream);
+
+/* Backward, Alg. 1 lines 9-15:
+ *   dÎ      = dO_local x W_{j,i}^T           (line 11)
+ *   dI      = all-reduce_x(dÎ)                (line 12; over Y if transposed),
+ *             overlapped with line 13 (OAR)
+ *   dWpart  = I_local^T x dO_local            (line 13)
+ *   dW_hat  = reduce-scatter_z(dWpart)        (line 14), NOT waited here (ORS,
+ *             PAPER.md:660-669): it completes at axonn_grads_sync
+ *   if Gd > 1: dW_hat += all-reduce over DATA (sum, R9),
+ *             issued right after this layer's reduce-scatter.
+ * dO_local [m_l][n_l], dI_local [m_l][k_l], dW_hat [what_len].  dI_local is
+ * ready in `stream` order when this call returns; dW_hat only after
+ * axonn_grads_sync(stream).  Errors: STATE (no forward since the last
+ * backward), ARG, CUDA, NCCL. */
+axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_local,
+                                 void* dW_hat, void* stream);
+
+/* The single ORS / data-parallel wait point: makes `stream` wait for every
+ * reduce-scatter and data-parallel all-reduce issued since the last call. */
+axonn_status_t axonn_grads_sync(void* stream);
+
+axonn_status_t axonn_fc_destroy(axonn_fc_t h);
+
+/* ======================================================================== */
+/* The three local products on the tensor cores (Alg. 1 lines 3, 11, 13),    */
+/* exposed for kernel parity tests and the GEMM-only timing of bench.py.     */
+/*   AXONN_OP_NN: C[M][N] = A[M][K]   x B[K][N]    (line 3:  I x W)           */
+/*   AXONN_OP_NT: C[M][N] = A[M][K]   x B[N][K]^T  (line 11: dO x W^T)        */
+/*   AXONN_OP_TN: C[M][N] = A[K][M]^T x B[K][N]    (line 13: I^T x dO)        */
+/* Row-major, leading dimensions lda/ldb/ldc in elements (multiples of 8 for */
+/* bf16, 16-byte aligned base pointers).  bf16: tcgen05.mma kind::f16 with   */
+/* fp32 accumulation in TMEM, one RNE rounding to bf16 at the end.  f32: SIMT*/
+/* fp32 FMA (test mode).  M, N, K >= 0 (K == 0 writes zeros).                */
+/* ======================================================================== */
+typedef enum { AXONN_OP_NN = 0, AXONN_OP_NT = 1, AXONN_OP_TN = 2 } axonn_op_t;
+
+axonn_status_t axonn_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K,
+                          const void* A, int64_t lda, const void* B, int64_t ldb,
+                          void* C, int64_t ldc, void* stream);
+
+/* ======================================================================== */
+/* Instrumentation: CUDA events around every GEMM launch on its launching    */
+/* stream, and a count of every kernel this library launched.                */
+/* ======================================================================== */
+axonn_status_t axonn_profile_enable(int enabled);
+/* Synchronises the recorded events; returns the number of GEMM launches, the
+ * summed GEMM device time (ms) and summed algorithmic flops (2*M*N*K) since
+ * the last reset, then resets. */
+axonn_status_t axonn_profile_read(int64_t* gemm_launches, double* gemm_ms, double* gemm_flops);
+/* Kernels launched by this library since load (GEMMs + helper kernels; NCCL
+ * kernels excluded). */
+int64_t axonn_kernel_launches(void);
+/* SM budget of the persistent GEMM grid (<= 0 or > #SMs: all SMs).  Leaving
+ * SMs free lets NCCL kernels run beside the GEMM when collectives overlap. */
+axonn_status_t axonn_set_gemm_sms(int sms);
+
+/* ======================================================================== */
+/* Performance model: Eqs. 1-6 per layer, summed over     */
+/* layers, with per-level bandwidths from the Case-1 table*/
+/* or Eq. 7, ranked ascending.         */
+/* ======================================================================== */
+typedef struct {
+  int64_t m, k, n;    /* m = global tokens (all replicas) */
+  int transposed;
+} axonn_layer_t;
+
+/* Case-1 database entry: groups of size G1 whose preceding hierarchy product
+ * is G0 achieve `bytes_per_s`. */
+typedef struct {
+  int inner;          /* G0 = prod_{j<i} G_j */
+  int size;           /* G1 = G_i            */
+  double bytes_per_s;
+} axonn_bw_entry_t;
+
+/* One ranked configuration.  t_ar_y / t_ar_x are the Eq. 3 / Eq. 4 terms
+ * (forward / backward-dI all-reduce) summed over layers after the transposed
+ * layers' X<->Y swap. */
+typedef struct {
+  int gx, gy, gz, gd;
+  double t_ag_z, t_rs_z, t_ar_y, t_ar_x, t_ar_data, t_comm;   /* seconds */
+} axonn_grid_score_t;
+
+/* Enumerate every (gx,gy,gz,gd) with product G (gd fixed when fixed_gd > 0),
+ * drop those that do not divide every layer, score by Eq. 6 summed over
+ * layers with b = bytes_per_elem, sort ascending with ties (relative 1e-12)
+ * broken lexicographically on (gx,gy,gz,gd) (reading R12), and write the
+ * first min(cap, count) to `out` (host).  *n_out = total feasible count.
+ * Errors: ARG, CONFIG (a needed Case-1 table entry is missing; the message
+ * names (G0,G1)), INFEASIBLE (no configuration). */
+axonn_status_t axonn_grid_select(const axonn_layer_t* layers, int n_layers, int G, int g_node,
+                                 const axonn_bw_entry_t* table, int n_table, double beta_inter,
+                                 int bytes_per_elem, int fixed_gd, axonn_grid_score_t* out,
+                                 int cap, int* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AXONN_H */

@@ -1,0 +1,683 @@
+// axonn.cpp — host runtime behind include/axonn.h.
+//
+// One process per GPU.  The runtime owns:
+//   * the world NCCL communicator and the four axis sub-communicators
+//     (X, Y, Z, DATA; ncclCommSplit with key = axis coordinate, so NCCL rank
+//     order is the coordinate order of PAPER.md:505-510);
+//   * one high-priority communication stream per axis;
+//   * layer handles (Alg. 1 state: cached I, gathered W, dW partial, events);
+//   * GEMM instrumentation (CUDA events on the launching stream).
+// Scheduling of one layer (Alg. 1, with the paper's overlap
+// optimisations PAPER.md:644-680):
+//   forward : [Z stream]  all-gather_z(W_hat) -> W          (OAG: may be prefetched)
+//             [caller]    wait AG; GEMM chunk c of I x W; record chunk event
+//             [fwd stream] per chunk: wait chunk event; all-reduce that chunk
+//             [caller]    wait last all-reduce
+//   backward: [caller]    GEMM dO x W^T -> dI
+//             [bwd stream] wait; all-reduce(dI)                (OAR, overlaps next GEMM)
+//             [caller]    GEMM I^T x dO -> dW partial
+//             [Z stream]  wait; reduce-scatter_z -> dW_hat     (ORS: not waited here)
+//             [D stream]  wait RS; all-reduce_data(dW_hat)     (per layer)
+//             [caller]    wait all-reduce(dI)
+//   grads_sync: caller waits every pending RS / DP all-reduce.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/axonn.h"
+#include "gemm.h"
+#include "perf_model.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+axonn_status_t fail(axonn_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(AXONN_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));         \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(AXONN_ERR_NCCL, "%s failed: %s", #expr, ncclGetErrorString(r_));         \
+  } while (0)
+
+#define STATUS_TRY(expr)                  \
+  do {                                    \
+    axonn_status_t s_ = (expr);           \
+    if (s_ != AXONN_OK) return s_;        \
+  } while (0)
+
+enum Axis { AX_X = 0, AX_Y = 1, AX_Z = 2, AX_D = 3 };
+
+struct ProfRec {
+  cudaEvent_t start, stop;
+  double flops;
+};
+
+struct State {
+  bool booted = false;
+  int rank = 0, world = 1, device = -1, num_sms = 0, gemm_sms = 0;
+  ncclComm_t world_comm = nullptr;
+  bool grid = false;
+  int g[4] = {1, 1, 1, 1};
+  int c[4] = {0, 0, 0, 0};
+  ncclComm_t axis_comm[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> pending_grads;
+  std::set<struct ::axonn_fc*> handles;
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_free;
+};
+
+State S;
+std::recursive_mutex g_mu;
+std::atomic<int64_t> g_launches{0};
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline size_t elem_size(int dtype) { return dtype == AXONN_F32 ? 4 : 2; }
+inline ncclDataType_t nccl_type(int dtype) {
+  return dtype == AXONN_F32 ? ncclFloat32 : ncclBfloat16;
+}
+
+// Fail loudly unless the current device is an sm_100 part (the kernels are
+// compiled for sm_100a only; there is no other path).
+axonn_status_t ensure_device() {
+  if (S.num_sms > 0) return AXONN_OK;
+  int dev = 0, major = 0, minor = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (major != 10 || minor != 0)
+    return fail(AXONN_ERR_CUDA, "libaxonn kernels are built for sm_100a; device %d is sm_%d%d",
+                dev, major, minor);
+  S.device = dev;
+  S.num_sms = sms;
+  if (S.gemm_sms <= 0 || S.gemm_sms > sms) S.gemm_sms = sms;
+  return AXONN_OK;
+}
+
+axonn_status_t check_async_nccl() {
+  for (int a = 0; a < 4; ++a) {
+    if (!S.axis_comm[a]) continue;
+    ncclResult_t ar = ncclSuccess;
+    NCCL_TRY(ncclCommGetAsyncError(S.axis_comm[a], &ar));
+    if (ar != ncclSuccess && ar != ncclInProgress)
+      return fail(AXONN_ERR_NCCL, "asynchronous NCCL error on axis %d: %s", a,
+                  ncclGetErrorString(ar));
+  }
+  return AXONN_OK;
+}
+
+// One local product on `st`, instrumented.  K == 0 writes zeros.
+axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                        int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                        cudaStream_t st) {
+  STATUS_TRY(ensure_device());
+  if (M == 0 || N == 0) return AXONN_OK;
+  const size_t es = elem_size(dtype);
+  if (K == 0) {
+    CUDA_TRY(cudaMemset2DAsync(C, ldc * es, 0, N * es, M, st));
+    return AXONN_OK;
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (S.profiling) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (!S.prof_free.empty()) {
+        *e = S.prof_free.back();
+        S.prof_free.pop_back();
+      } else {
+        CUDA_TRY(cudaEventCreate(e));
+      }
+    }
+    CUDA_TRY(cudaEventRecord(e0, st));
+  }
+  axonn::GemmStatus gs;
+  if (dtype == AXONN_BF16)
+    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st);
+  else
+    gs = axonn::gemm_f32_simt(op, M, N, K, static_cast<const float*>(A), lda,
+                              static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc, st);
+  switch (gs) {
+    case axonn::GemmStatus::kOk: break;
+    case axonn::GemmStatus::kBadAlignment:
+      return fail(AXONN_ERR_ARG, "gemm: bf16 operands need 16-byte aligned bases and ld %% 8 == 0");
+    case axonn::GemmStatus::kBadShape:
+      return fail(AXONN_ERR_SHAPE, "gemm: dimension exceeds 2^31-1");
+    case axonn::GemmStatus::kTensorMap:
+      return fail(AXONN_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+    case axonn::GemmStatus::kBadOp:
+      return fail(AXONN_ERR_ARG, "gemm: op must be 0 (NN), 1 (NT) or 2 (TN)");
+    default: {
+      cudaError_t e = cudaGetLastError();
+      return fail(AXONN_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(e));
+    }
+  }
+  g_launches.fetch_add(1);
+  if (S.profiling) {
+    CUDA_TRY(cudaEventRecord(e1, st));
+    S.prof.push_back({e0, e1, 2.0 * static_cast<double>(M) * N * K});
+  }
+  return AXONN_OK;
+}
+
+int coords_to_rank(const int g[4], const int c[4]) {
+  return c[0] + g[0] * (c[1] + g[1] * (c[2] + g[2] * c[3]));
+}
+
+axonn_status_t check_grid_args(int gx, int gy, int gz, int gd) {
+  if (gx < 1 || gy < 1 || gz < 1 || gd < 1)
+    return fail(AXONN_ERR_CONFIG, "configuration error: factors (%d,%d,%d,%d) must be >= 1", gx,
+                gy, gz, gd);
+  return AXONN_OK;
+}
+
+axonn_status_t geometry_of(const axonn_fc_desc_t* d, const int g[4], int rank,
+                           axonn_geometry_t* out) {
+  if (!d || !out) return fail(AXONN_ERR_ARG, "NULL argument");
+  if (d->m < 0 || d->k < 0 || d->n < 0) return fail(AXONN_ERR_ARG, "negative dimension");
+  if (d->dtype != AXONN_BF16 && d->dtype != AXONN_F32)
+    return fail(AXONN_ERR_ARG, "dtype must be AXONN_BF16 or AXONN_F32");
+  const int G = g[0] * g[1] * g[2] * g[3];
+  if (rank < 0 || rank >= G) return fail(AXONN_ERR_ARG, "rank %d outside grid of %d", rank, G);
+  const bool t = d->transposed != 0;
+  const int ga = t ? g[AX_X] : g[AX_Y];
+  const int gb = t ? g[AX_Y] : g[AX_X];
+  const char* na = t ? "Gx" : "Gy";
+  const char* nb = t ? "Gy" : "Gx";
+  const int64_t zd = static_cast<int64_t>(g[AX_Z]) * g[AX_D];
+  if (d->m % zd)
+    return fail(AXONN_ERR_SHAPE, "m=%lld not divisible by Gz*Gd=%lld", (long long)d->m,
+                (long long)zd);
+  if (d->k % ga) return fail(AXONN_ERR_SHAPE, "k=%lld not divisible by %s=%d", (long long)d->k, na, ga);
+  if (d->n % gb) return fail(AXONN_ERR_SHAPE, "n=%lld not divisible by %s=%d", (long long)d->n, nb, gb);
+  const int64_t k_l = d->k / ga, n_l = d->n / gb;
+  if ((k_l * n_l) % g[AX_Z])
+    return fail(AXONN_ERR_SHAPE, "k_l*n_l=%lld not divisible by Gz=%d", (long long)(k_l * n_l),
+                g[AX_Z]);
+  int c[4];
+  int r = rank;
+  for (int a = 0; a < 4; ++a) {
+    c[a] = r % g[a];
+    r /= g[a];
+  }
+  const int ia = t ? c[AX_X] : c[AX_Y];  // contraction-block index
+  const int ib = t ? c[AX_Y] : c[AX_X];  // output-column-block index
+  out->m_l = d->m / zd;
+  out->k_l = k_l;
+  out->n_l = n_l;
+  out->row0 = (static_cast<int64_t>(c[AX_D]) * g[AX_Z] + c[AX_Z]) * out->m_l;
+  out->in_col0 = ia * k_l;
+  out->out_col0 = ib * n_l;
+  out->what_len = k_l * n_l / g[AX_Z];
+  out->what_off = c[AX_Z] * out->what_len;
+  return AXONN_OK;
+}
+
+}  // namespace
+
+// ============================================================== layer handle
+struct axonn_fc {
+  axonn_fc_desc_t d;
+  axonn_geometry_t geo;
+  int ax_fwd, ax_bwd;         // axis of the forward / backward-dI all-reduce
+  void* wbuf = nullptr;       // gathered W_{j,i} when Gz > 1
+  void* dwpart = nullptr;     // dW partial when Gz > 1
+  const void* I = nullptr;    // cached I_{k,j} (caller-owned)
+  const void* W = nullptr;    // W_{j,i} used by the last forward
+  bool have_fwd = false;
+  bool prefetched = false;
+  cudaEvent_t ev_in = nullptr, ev_ag = nullptr, ev_ar = nullptr, ev_dw = nullptr,
+              ev_rs = nullptr, ev_grad = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
+};
+
+namespace {
+
+axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) {
+  if (S.g[AX_Z] == 1) {
+    h->prefetched = true;
+    return AXONN_OK;
+  }
+  const size_t S_el = static_cast<size_t>(h->geo.what_len);
+  CUDA_TRY(cudaEventRecord(h->ev_in, st));
+  CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_in, 0));
+  NCCL_TRY(ncclAllGather(W_hat, h->wbuf, S_el, nccl_type(h->d.dtype), S.axis_comm[AX_Z],
+                         S.cstream[AX_Z]));
+  CUDA_TRY(cudaEventRecord(h->ev_ag, S.cstream[AX_Z]));
+  h->prefetched = true;
+  return AXONN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* axonn_last_error(void) { return g_err.c_str(); }
+int axonn_version(void) { return 100; }
+
+axonn_status_t axonn_unique_id(unsigned char id[128]) {
+  if (!id) return fail(AXONN_ERR_ARG, "NULL id");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  ncclUniqueId uid;
+  NCCL_TRY(ncclGetUniqueId(&uid));
+  std::memcpy(id, &uid, 128);
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_bootstrap(int world_rank, int world_size, const unsigned char* id,
+                               int cuda_device) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (S.booted) return fail(AXONN_ERR_STATE, "already bootstrapped");
+  if (world_size < 1 || world_rank < 0 || world_rank >= world_size || cuda_device < 0)
+    return fail(AXONN_ERR_ARG, "bad rank/world/device (%d/%d/%d)", world_rank, world_size,
+                cuda_device);
+  if (world_size > 1 && !id) return fail(AXONN_ERR_ARG, "world_size > 1 needs an NCCL id");
+  CUDA_TRY(cudaSetDevice(cuda_device));
+  S.num_sms = 0;
+  STATUS_TRY(ensure_device());
+  if (world_size > 1) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    NCCL_TRY(ncclCommInitRankConfig(&S.world_comm, world_size, uid, world_rank, &cfg));
+  }
+  S.rank = world_rank;
+  S.world = world_size;
+  S.booted = true;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_rank_to_coords(int rank, int gx, int gy, int gz, int gd, int coords[4]) {
+  STATUS_TRY(check_grid_args(gx, gy, gz, gd));
+  if (!coords) return fail(AXONN_ERR_ARG, "NULL coords");
+  const int g[4] = {gx, gy, gz, gd};
+  if (rank < 0 || rank >= gx * gy * gz * gd) return fail(AXONN_ERR_ARG, "rank out of range");
+  int r = rank;
+  for (int a = 0; a < 4; ++a) {
+    coords[a] = r % g[a];
+    r /= g[a];
+  }
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_group_members(int rank, int gx, int gy, int gz, int gd, int axis,
+                                   int* members) {
+  int c[4];
+  STATUS_TRY(axonn_rank_to_coords(rank, gx, gy, gz, gd, c));
+  if (axis < 0 || axis > 3 || !members) return fail(AXONN_ERR_ARG, "bad axis or NULL members");
+  const int g[4] = {gx, gy, gz, gd};
+  for (int v = 0; v < g[axis]; ++v) {
+    int cc[4] = {c[0], c[1], c[2], c[3]};
+    cc[axis] = v;
+    members[v] = coords_to_rank(g, cc);
+  }
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  STATUS_TRY(check_grid_args(gx, gy, gz, gd));
+  const int G = gx * gy * gz * gd;
+  if (S.grid) return fail(AXONN_ERR_STATE, "grid already initialised; call axonn_grid_finalize");
+  if (!S.booted) {
+    if (G != 1)
+      return fail(AXONN_ERR_STATE, "axonn_bootstrap must precede a grid of %d ranks", G);
+    S.rank = 0;  // single-GPU: bind to the current device, no communicator
+    S.world = 1;
+    S.num_sms = 0;
+    STATUS_TRY(ensure_device());
+    S.booted = true;
+  }
+  if (G != S.world)
+    return fail(AXONN_ERR_CONFIG, "configuration error: gx*gy*gz*gd = %d != world size %d", G,
+                S.world);
+  const int g[4] = {gx, gy, gz, gd};
+  std::memcpy(S.g, g, sizeof g);
+  STATUS_TRY(axonn_rank_to_coords(S.rank, gx, gy, gz, gd, S.c));
+  int lo = 0, hi = 0;
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  for (int a = 0; a < 4; ++a) {
+    if (g[a] > 1) {
+      int cc[4] = {S.c[0], S.c[1], S.c[2], S.c[3]};
+      cc[a] = 0;
+      const int color = coords_to_rank(g, cc);
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      NCCL_TRY(ncclCommSplit(S.world_comm, color, S.c[a], &S.axis_comm[a], &cfg));
+    }
+    CUDA_TRY(cudaStreamCreateWithPriority(&S.cstream[a], cudaStreamNonBlocking, hi));
+  }
+  S.grid = true;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_grid_coords(int* i, int* j, int* k, int* d) {
+  if (!S.grid) return fail(AXONN_ERR_STATE, "no grid");
+  if (!i || !j || !k || !d) return fail(AXONN_ERR_ARG, "NULL argument");
+  *i = S.c[0];
+  *j = S.c[1];
+  *k = S.c[2];
+  *d = S.c[3];
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fc_destroy(axonn_fc_t h);
+
+axonn_status_t axonn_grid_finalize(void) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!S.grid) return AXONN_OK;
+  std::vector<axonn_fc*> hs(S.handles.begin(), S.handles.end());
+  for (auto* h : hs) axonn_fc_destroy(h);
+  for (int a = 0; a < 4; ++a) {
+    if (S.cstream[a]) cudaStreamSynchronize(S.cstream[a]);
+    if (S.axis_comm[a]) ncclCommDestroy(S.axis_comm[a]);
+    if (S.cstream[a]) cudaStreamDestroy(S.cstream[a]);
+    S.axis_comm[a] = nullptr;
+    S.cstream[a] = nullptr;
+  }
+  S.pending_grads.clear();
+  S.grid = false;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_shard_geometry(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
+                                    int rank, axonn_geometry_t* out) {
+  STATUS_TRY(check_grid_args(gx, gy, gz, gd));
+  const int g[4] = {gx, gy, gz, gd};
+  return geometry_of(desc, g, rank, out);
+}
+
+axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!desc || !out) return fail(AXONN_ERR_ARG, "NULL argument");
+  if (!S.grid) return fail(AXONN_ERR_STATE, "axonn_grid_init must precede axonn_fc_create");
+  axonn_geometry_t geo;
+  STATUS_TRY(geometry_of(desc, S.g, S.rank, &geo));
+  auto* h = new axonn_fc();
+  h->d = *desc;
+  if (h->d.chunks < 1) h->d.chunks = 1;
+  h->geo = geo;
+  h->ax_fwd = desc->transposed ? AX_X : AX_Y;
+  h->ax_bwd = desc->transposed ? AX_Y : AX_X;
+  const size_t wbytes = static_cast<size_t>(geo.k_l) * geo.n_l * elem_size(desc->dtype);
+  auto cleanup = [&](axonn_status_t s) {
+    axonn_fc_destroy(h);
+    return s;
+  };
+  S.handles.insert(h);
+  if (S.g[AX_Z] > 1 && wbytes) {
+    if (cudaMalloc(&h->wbuf, wbytes) != cudaSuccess || cudaMalloc(&h->dwpart, wbytes) != cudaSuccess)
+      return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", 2 * wbytes));
+  }
+  for (cudaEvent_t* e : {&h->ev_in, &h->ev_ag, &h->ev_ar, &h->ev_dw, &h->ev_rs, &h->ev_grad})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
+  h->ev_chunk.resize(h->d.chunks + 1, nullptr);
+  for (auto& e : h->ev_chunk)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
+  *out = h;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out) {
+  if (!h || !out) return fail(AXONN_ERR_ARG, "NULL argument");
+  *out = h->geo;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fc_prefetch(axonn_fc_t h, const void* W_hat, void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!h || (!W_hat && h->geo.what_len)) return fail(AXONN_ERR_ARG, "NULL argument");
+  if (!S.grid) return fail(AXONN_ERR_STATE, "no grid");
+  return issue_allgather(h, W_hat, as_stream(stream));
+}
+
+axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W_hat,
+                                void* O_local, void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!h) return fail(AXONN_ERR_ARG, "NULL handle");
+  if (!S.grid) return fail(AXONN_ERR_STATE, "no grid");
+  const axonn_geometry_t& g = h->geo;
+  if ((!I_local && (g.m_l * g.k_l) != 0) || (!W_hat && g.what_len != 0) || (!O_local && (g.m_l * g.n_l) != 0))
+    return fail(AXONN_ERR_ARG, "NULL tensor");
+  STATUS_TRY(check_async_nccl());
+  cudaStream_t st = as_stream(stream);
+  // line 2: W_{j,i} = all-gather_z(W_hat)
+  if (!h->prefetched) STATUS_TRY(issue_allgather(h, W_hat, st));
+  h->prefetched = false;
+  const void* W = S.g[AX_Z] > 1 ? h->wbuf : W_hat;
+  if (S.g[AX_Z] > 1) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ag, 0));
+  // line 3 + line 4, pipelined over M-chunks when requested
+  const int P = S.g[h->ax_fwd];
+  const size_t es = elem_size(h->d.dtype);
+  int chunks = (P > 1) ? h->d.chunks : 1;
+  int64_t rows_per = (g.m_l + chunks - 1) / chunks;
+  rows_per = (rows_per + 127) / 128 * 128;  // whole 128-row GEMM tiles per chunk
+  if (rows_per <= 0) rows_per = 1;
+  cudaStream_t cs = S.cstream[h->ax_fwd];
+  int c = 0;
+  for (int64_t r0 = 0; r0 < g.m_l || (g.m_l == 0 && c == 0); r0 += rows_per, ++c) {
+    const int64_t rows = std::min<int64_t>(rows_per, g.m_l - r0);
+    const char* Ic = static_cast<const char*>(I_local) + r0 * g.k_l * es;
+    char* Oc = static_cast<char*>(O_local) + r0 * g.n_l * es;
+    STATUS_TRY(run_gemm(AXONN_OP_NN, h->d.dtype, rows, g.n_l, g.k_l, Ic, g.k_l, W, g.n_l, Oc,
+                        g.n_l, st));
+    if (P > 1 && rows > 0) {
+      cudaEvent_t ev = h->ev_chunk[std::min<size_t>(c, h->ev_chunk.size() - 1)];
+      CUDA_TRY(cudaEventRecord(ev, st));
+      CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
+      NCCL_TRY(ncclAllReduce(Oc, Oc, static_cast<size_t>(rows * g.n_l), nccl_type(h->d.dtype),
+                             ncclSum, S.axis_comm[h->ax_fwd], cs));
+    }
+    if (g.m_l == 0) break;
+  }
+  if (P > 1) {
+    CUDA_TRY(cudaEventRecord(h->ev_ar, cs));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ar, 0));
+  }
+  // line 5: cache I_{k,j} and W_{j,i}
+  h->I = I_local;
+  h->W = W;
+  h->have_fwd = true;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_local,
+                                 void* dW_hat, void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!h) return fail(AXONN_ERR_ARG, "NULL handle");
+  if (!S.grid) return fail(AXONN_ERR_STATE, "no grid");
+  if (!h->have_fwd) return fail(AXONN_ERR_STATE, "axonn_fc_backward before axonn_fc_forward");
+  const axonn_geometry_t& g = h->geo;
+  if ((!dO_local && (g.m_l * g.n_l) != 0) || (!dI_local && (g.m_l * g.k_l) != 0) || (!dW_hat && g.what_len != 0))
+    return fail(AXONN_ERR_ARG, "NULL tensor");
+  STATUS_TRY(check_async_nccl());
+  cudaStream_t st = as_stream(stream);
+  const int dt = h->d.dtype;
+  const ncclDataType_t nt = nccl_type(dt);
+  // line 11: dI^ = dO x W^T       (M = m_l, N = k_l, K = n_l)
+  STATUS_TRY(run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
+                      dI_local, g.k_l, st));
+  // line 12: dI = all-reduce_x(dI^), overlapped with line 13 (OAR)
+  const int Pb = S.g[h->ax_bwd];
+  cudaStream_t bs = S.cstream[h->ax_bwd];
+  if (Pb > 1) {
+    CUDA_TRY(cudaEventRecord(h->ev_dw, st));
+    CUDA_TRY(cudaStreamWaitEvent(bs, h->ev_dw, 0));
+    NCCL_TRY(ncclAllReduce(dI_local, dI_local, static_cast<size_t>((g.m_l * g.k_l) != 0), nt, ncclSum,
+                           S.axis_comm[h->ax_bwd], bs));
+    CUDA_TRY(cudaEventRecord(h->ev_ar, bs));
+  }
+  // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
+  const bool rs = S.g[AX_Z] > 1;
+  void* dst = rs ? h->dwpart : dW_hat;
+  STATUS_TRY(run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst,
+                      g.n_l, st));
+  // line 14: dW_hat = reduce-scatter_z(dW partial)   (ORS: waited in grads_sync)
+  const size_t S_el = static_cast<size_t>(g.what_len != 0);
+  cudaEvent_t last = nullptr;
+  if (rs) {
+    CUDA_TRY(cudaEventRecord(h->ev_rs, st));
+    CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
+    NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_Z],
+                               S.cstream[AX_Z]));
+    CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_Z]));
+    last = h->ev_grad;
+  }
+  // data parallelism: sum dW_hat over the replicas, per layer
+  if (S.g[AX_D] > 1) {
+    CUDA_TRY(cudaEventRecord(h->ev_rs, rs ? S.cstream[AX_Z] : st));
+    CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_D], h->ev_rs, 0));
+    NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_D],
+                           S.cstream[AX_D]));
+    CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_D]));
+    last = h->ev_grad;
+  }
+  if (last) {
+    bool seen = false;
+    for (auto e : S.pending_grads) seen = seen || (e == last);
+    if (!seen) S.pending_grads.push_back(last);
+  }
+  // dI must be complete in `stream` order when we return
+  if (Pb > 1) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ar, 0));
+  h->have_fwd = false;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_grads_sync(void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  cudaStream_t st = as_stream(stream);
+  for (auto e : S.pending_grads) CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
+  S.pending_grads.clear();
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!h) return AXONN_OK;
+  if (!S.handles.count(h)) return fail(AXONN_ERR_ARG, "unknown handle");
+  S.handles.erase(h);
+  cudaDeviceSynchronize();
+  for (cudaEvent_t e : {h->ev_in, h->ev_ag, h->ev_ar, h->ev_dw, h->ev_rs, h->ev_grad}) {
+    if (!e) continue;
+    for (size_t i = 0; i < S.pending_grads.size(); ++i)
+      if (S.pending_grads[i] == e) S.pending_grads.erase(S.pending_grads.begin() + i--);
+    cudaEventDestroy(e);
+  }
+  for (auto e : h->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (h->wbuf) cudaFree(h->wbuf);
+  if (h->dwpart) cudaFree(h->dwpart);
+  delete h;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                          int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                          void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (op < 0 || op > 2) return fail(AXONN_ERR_ARG, "op must be 0 (NN), 1 (NT) or 2 (TN)");
+  if (dtype != AXONN_BF16 && dtype != AXONN_F32) return fail(AXONN_ERR_ARG, "bad dtype");
+  if (M < 0 || N < 0 || K < 0) return fail(AXONN_ERR_ARG, "negative dimension");
+  if (M && N && (!C || (K && (!A || !B)))) return fail(AXONN_ERR_ARG, "NULL matrix");
+  const int64_t a_cols = (op == AXONN_OP_TN) ? M : K;
+  const int64_t b_cols = (op == AXONN_OP_NT) ? K : N;
+  if ((K && M && lda < a_cols) || (K && N && ldb < b_cols) || (M && ldc < N))
+    return fail(AXONN_ERR_ARG, "leading dimension smaller than the row length");
+  return run_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, as_stream(stream));
+}
+
+axonn_status_t axonn_profile_enable(int enabled) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  S.profiling = enabled != 0;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_profile_read(int64_t* launches, double* ms, double* flops) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!launches || !ms || !flops) return fail(AXONN_ERR_ARG, "NULL argument");
+  *launches = 0;
+  *ms = 0.0;
+  *flops = 0.0;
+  for (auto& p : S.prof) {
+    CUDA_TRY(cudaEventSynchronize(p.stop));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, p.start, p.stop));
+    *ms += t;
+    *flops += p.flops;
+    *launches += 1;
+    S.prof_free.push_back(p.start);
+    S.prof_free.push_back(p.stop);
+  }
+  S.prof.clear();
+  return AXONN_OK;
+}
+
+int64_t axonn_kernel_launches(void) { return g_launches.load(); }
+
+axonn_status_t axonn_set_gemm_sms(int sms) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  STATUS_TRY(ensure_device());
+  S.gemm_sms = (sms <= 0 || sms > S.num_sms) ? S.num_sms : sms;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_grid_select(const axonn_layer_t* layers, int n_layers, int G, int g_node,
+                                 const axonn_bw_entry_t* table, int n_table, double beta_inter,
+                                 int bytes_per_elem, int fixed_gd, axonn_grid_score_t* out,
+                                 int cap, int* n_out) {
+  if ((!layers && n_layers) || n_layers < 0 || G < 1 || g_node < 1 || (!table && n_table) ||
+      n_table < 0 || !(beta_inter > 0) || bytes_per_elem < 1 || cap < 0 || (!out && cap) || !n_out)
+    return fail(AXONN_ERR_ARG, "bad argument to axonn_grid_select");
+  std::vector<axonn::Layer> ls;
+  for (int i = 0; i < n_layers; ++i) {
+    if (layers[i].m < 0 || layers[i].k < 0 || layers[i].n < 0)
+      return fail(AXONN_ERR_ARG, "negative layer dimension");
+    ls.push_back({layers[i].m, layers[i].k, layers[i].n, layers[i].transposed != 0});
+  }
+  std::vector<axonn::BwEntry> tb;
+  for (int i = 0; i < n_table; ++i) {
+    if (!(table[i].bytes_per_s > 0)) return fail(AXONN_ERR_ARG, "bandwidth must be > 0");
+    tb.push_back({table[i].inner, table[i].size, table[i].bytes_per_s});
+  }
+  std::vector<axonn::Scored> ranked;
+  std::string err;
+  const int n = axonn::rank_configs(ls, G, g_node, tb, beta_inter, bytes_per_elem, fixed_gd,
+                                    &ranked, &err);
+  if (n < 0) return fail(AXONN_ERR_CONFIG, "configuration error: %s", err.c_str());
+  *n_out = n;
+  if (n == 0) return fail(AXONN_ERR_INFEASIBLE, "infeasible: no configuration of %d GPUs divides every layer", G);
+  for (int i = 0; i < n && i < cap; ++i) {
+    const auto& s = ranked[i];
+    out[i] = {s.c.gx, s.c.gy, s.c.gz, s.c.gd, s.t.ag_z, s.t.rs_z,
+              s.t.ar_y, s.t.ar_x, s.t.ar_d, s.t.comm};
+  }
+  return AXONN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+// gemm_tc.cu — the three local products of Algorithm 1 on the sm_100a tensor cores.
+//
+//   line 3  O^  = I  x W     -> op NN: A K-major,  B MN-major
+//   line 11  dI^ = dO x W^T   -> op NT: A K-major,  B K-major
+//   line 13  dW  = I^T x dO   -> op TN: A MN-major, B MN-major
+//
+// The paper tuned cuBLAS/rocBLAS NN/NT/TN modes because its
+// TN kernel ran at 6% of peak.  On tcgen05 the operand major is two bits of the
+// instruction descriptor, so all three products are one kernel template that
+// stages operands with TMA in the layout they already have in HBM — no
+// transposes, no mode tuner.
+//
+// Kernel: persistent, warp-specialised, one CTA per SM.
+//   warp 0      TMA producer   (one elected lane): A/B tiles -> smem ring
+//   warp 1      MMA issuer     (one lane): tcgen05.mma 128x256x16, fp32 in TMEM
+//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7  epilogue: tcgen05.ld -> RNE bf16 -> global, overlapping the next
+//               tile's main loop (double-buffered accumulator)
+// Tiles: BM=128, BN=256, BK=64 (one 128-byte swizzle row of bf16), 4 stages.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace axonn {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int THREADS = 256;
+constexpr int SMEM_A = BM * BK * 2;  // 16 KiB
+constexpr int SMEM_B = BN * BK * 2;  // 32 KiB
+constexpr int STAGE_BYTES = SMEM_A + SMEM_B;
+constexpr int TMEM_COLS = 2 * BN;    // two fp32 accumulators
+constexpr int MN_CHUNK = 64;         // MN-major operands: 64-element (128 B) chunks
+constexpr int MN_CHUNK_BYTES = MN_CHUNK * BK * 2;  // 8 KiB, the LBO of MN-major tiles
+constexpr int GROUP_M = 16;          // tile raster: bands of 16 M-tiles for L2 reuse
+constexpr size_t SMEM_BYTES = 1024 /*align*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+struct TileCoord {
+  int m0, n0;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n) {
+  const int per_group = GROUP_M * tiles_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int r = t - g * per_group;
+  return {(first_m + r % gm) * BM, (r / gm) * BN};
+}
+
+// A_MN / B_MN: 0 = operand stored K-major in HBM, 1 = stored MN-major.
+template <int A_MN, int B_MN>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, __nv_bfloat16* __restrict__ C,
+                      int64_t ldc, int M, int N, int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * SMEM_A;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * SMEM_B);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tiles_m = (M + BM - 1) / BM;
+  const int tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(t, tiles_m, tiles_n);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* a_dst = sA + stage * SMEM_A;
+          uint8_t* b_dst = sB + stage * SMEM_B;
+          if (A_MN == 0) {
+            ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, tc.m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / MN_CHUNK; ++c)
+              ptx::tma_load_2d(a_dst + c * MN_CHUNK_BYTES, &tmA, &full[stage], tc.m0 + c * MN_CHUNK, k0);
+          }
+          if (B_MN == 0) {
+            ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, tc.n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / MN_CHUNK; ++c)
+              ptx::tma_load_2d(b_dst + c * MN_CHUNK_BYTES, &tmB, &full[stage], tc.n0 + c * MN_CHUNK, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sA + stage * SMEM_A);
+          const uint32_t b_base = ptx::smem_u32(sB + stage * SMEM_B);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major: advance 16 elements = 32 B inside the 128-B swizzle row.
+            // MN-major: advance 16 K-rows = two 1024-B swizzle atoms.
+            const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_base + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                     : ptx::sdesc_sw128(a_base + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                     : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
+            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);      // accumulator complete
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // --------------------------------------------------------- epilogue
+    const int e = warp - 4;  // TMEM lanes 32e .. 32e+31 (warp % 4 == e)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const TileCoord tc = tile_coord(t, tiles_m, tiles_n);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = tc.m0 + 32 * e + lane;
+      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) +
+                               static_cast<uint32_t>(acc * BN + c * 32);
+        ptx::tmem_ld_32x32b_x32(taddr, v);
+        ptx::tmem_wait_ld();
+        const int col0 = tc.n0 + c * 32;
+        if (row < M && col0 < N) {
+          if (vec_ok && col0 + 32 <= N) {
+            uint4* dst = reinterpret_cast<uint4*>(crow + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 w;
+              w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+              w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+              w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+              w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+              dst[q] = w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (col0 + q < N) crow[col0 + q] = __float2bfloat16_rn(__uint_as_float(v[q]));
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D bf16 tensor map over a row-major matrix: `inner` contiguous elements per
+// row, `outer` rows, row stride `ld` elements; box box_inner x box_outer with
+// 128-byte swizzle; out-of-bounds elements read as zero.
+bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int A_MN, int B_MN>
+cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M,
+                   int N, int K, int num_sms, cudaStream_t stream) {
+  auto kern = gemm_bf16_tcgen05<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  kern<<<grid, THREADS, SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M, N,
+                                              K);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// C[M][N] (bf16, ldc) = op(A) x op(B); see axonn_gemm in include/axonn.h.
+GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
+                        cudaStream_t stream) {
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return GemmStatus::kBadShape;
+  if ((lda & 7) || (ldb & 7) || (reinterpret_cast<uintptr_t>(A) & 15) ||
+      (reinterpret_cast<uintptr_t>(B) & 15))
+    return GemmStatus::kBadAlignment;
+  CUtensorMap ma, mb;
+  bool ok = true;
+  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+  cudaError_t e = cudaSuccess;
+  switch (op) {
+    case 0:  // NN: A [M][K], B [K][N]
+      ok = make_map(&ma, A, K, M, lda, BK, BM) && make_map(&mb, B, N, K, ldb, MN_CHUNK, BK);
+      if (!ok) return GemmStatus::kTensorMap;
+      e = launch<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
+      break;
+    case 1:  // NT: A [M][K], B [N][K]
+      ok = make_map(&ma, A, K, M, lda, BK, BM) && make_map(&mb, B, K, N, ldb, BK, BN);
+      if (!ok) return GemmStatus::kTensorMap;
+      e = launch<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream);
+      break;
+    case 2:  // TN: A [K][M], B [K][N]
+      ok = make_map(&ma, A, M, K, lda, MN_CHUNK, BK) && make_map(&mb, B, N, K, ldb, MN_CHUNK, BK);
+      if (!ok) return GemmStatus::kTensorMap;
+      e = launch<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
+      break;
+    default:
+      return GemmStatus::kBadOp;
+  }
+  return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
+}
+
+}  // namespace axonn

@@ -1,0 +1,98 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/axonn.h
+declares, and its pure-host logic (grid bijection, groups, shard geometry,
+performance model) agrees with the oracle.  No compute calls (no GPU here)."""
+import os
+import re
+
+import pytest
+
+import paper_2502_08145_b200 as ax
+from oracle import alg1, grid, perf_model as pm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "axonn.h")).read()
+    return sorted(set(re.findall(r"\b(axonn_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported_and_bound():
+    syms = _header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(ax._lib, s), s            # exported by libaxonn.so
+        assert s in ax.EXPORTED, s               # bound with a prototype in the binding
+        assert hasattr(ax, s), s                 # same name in Python
+
+
+def test_version_and_error_string():
+    assert ax.axonn_version() >= 100
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_rank_to_coords(0, (0, 1, 1, 1))
+    assert e.value.status == ax.AXONN_ERR_CONFIG
+    assert "configuration error" in ax.axonn_last_error()
+
+
+@pytest.mark.parametrize("cfg", [(2, 2, 2, 2), (1, 4, 2, 1), (3, 1, 2, 2), (1, 1, 1, 1)])
+def test_coords_and_groups_match_oracle(cfg):
+    G = cfg[0] * cfg[1] * cfg[2] * cfg[3]
+    for r in range(G):
+        assert ax.axonn_rank_to_coords(r, cfg) == grid.rank_to_coords(r, cfg)
+        for a in "xyzd":
+            assert ax.axonn_group_members(r, cfg, a) == grid.group_of(r, cfg, a)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+def test_shard_geometry_matches_oracle(transposed):
+    m, k, n = 96, 48, 72
+    for G in (1, 2, 4, 8, 12):
+        for cfg in grid.enumerate_configs(G):
+            if not pm.feasible(pm.Layer(m, k, n, transposed), cfg):
+                with pytest.raises(ax.AxonnError) as e:
+                    ax.axonn_shard_geometry(m, k, n, cfg, 0, transposed)
+                assert e.value.status == ax.AXONN_ERR_SHAPE
+                continue
+            for r in range(G):
+                g = ax.axonn_shard_geometry(m, k, n, cfg, r, transposed)
+                o = alg1.geometry(m, k, n, cfg, r, transposed)
+                assert tuple(g) == (o.m_l, o.k_l, o.n_l, o.row0, o.in_col0, o.out_col0,
+                                    o.what_off, o.what_len)
+
+
+def test_shape_error_names_axis():
+    with pytest.raises(ax.AxonnError, match="Gy"):
+        ax.axonn_shard_geometry(8, 5, 8, (1, 2, 1, 1), 0)
+
+
+def _table(g_node):
+    # a non-uniform Case-1 database: bandwidth falls with group size and depth
+    return {(g0, g1): 400e9 / (g1 ** 0.5) / (1 + 0.1 * g0)
+            for g0 in range(1, g_node + 1) for g1 in range(2, g_node + 1) if g0 * g1 <= g_node}
+
+
+@pytest.mark.parametrize("G,g_node,h,phase,gd", [(8, 8, 12288, "A", 1), (8, 8, 7168, "B", 0),
+                                                 (16, 4, 9216, "A", 0), (32, 4, 7168, "A", 1),
+                                                 (4, 8, 4096, "A", 0), (2, 8, 4096, "B", 0),
+                                                 (64, 8, 16384, "A", 0)])
+def test_grid_select_matches_oracle(G, g_node, h, phase, gd):
+    layers = pm.gpt_block(h, 16384, phase)
+    tb = _table(g_node)
+    want = pm.rank_configs(layers, G, g_node, tb, 25e9, b=2, fixed_gd=gd)
+    got = ax.axonn_grid_select([(L.m, L.k, L.n, L.transposed) for L in layers], G, g_node, tb,
+                               25e9, 2, gd)
+    assert [(r["gx"], r["gy"], r["gz"], r["gd"]) for r in got] == [c for c, _ in want]
+    for r, (_, t) in zip(got, want):
+        for key, ok in (("t_ag_z", "ag_z"), ("t_rs_z", "rs_z"), ("t_ar_y", "ar_y"),
+                        ("t_ar_x", "ar_x"), ("t_ar_data", "ar_d"), ("t_comm", "comm")):
+            assert r[key] == pytest.approx(float(t[ok]), rel=1e-12, abs=0)
+
+
+def test_grid_select_errors():
+    L = [(3, 5, 7, False)]
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_grid_select(L, 2, 8, pm.uniform_table(8, 1e9), 1e9)
+    assert e.value.status == ax.AXONN_ERR_INFEASIBLE
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_grid_select([(64, 64, 64, False)], 4, 8, {}, 1e9)
+    assert e.value.status == ax.AXONN_ERR_CONFIG and "G0=1, G1=" in str(e.value)

@@ -1,0 +1,88 @@
+"""Alg. 1 through the C ABI on one GPU (grid 1x1x1x1, BASELINE.json C2's grid):
+axonn_fc_forward / axonn_fc_backward / axonn_grads_sync against oracle.fc."""
+import numpy as np
+import pytest
+
+import synthdata
+from oracle import fc
+from gpu_util import bf16_bits_of, empty_dev, normwise_err, require_cuda, to_dev, to_host_f64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ax():
+    require_cuda()
+    import paper_2502_08145_b200 as ax
+    try:
+        ax.axonn_grid_init(1, 1, 1, 1)
+    except ax.AxonnError as e:            # another module already created the grid
+        assert e.status == ax.AXONN_ERR_STATE
+    yield ax
+
+
+def _layer(ax, m, k, n, transposed, kind, dtype_t, layer_id=0):
+    torch = require_cuda()
+    X, W, dY = synthdata.layer_tensors(m, k, n, layer_id, kind=kind)
+    dt = ax.AXONN_F32 if dtype_t == torch.float32 else ax.AXONN_BF16
+    h = ax.axonn_fc_create(m, k, n, transposed, dt)
+    g = ax.axonn_fc_geometry(h)
+    assert (g.m_l, g.k_l, g.n_l, g.what_len) == (m, k, n, k * n)
+    I = to_dev(X, dtype_t)
+    What = to_dev(W.reshape(1, -1), dtype_t).reshape(-1)
+    dO = to_dev(dY, dtype_t)
+    O = empty_dev(m, n, dtype_t)
+    dI = empty_dev(m, k, dtype_t)
+    dW = empty_dev(1, k * n, dtype_t).reshape(-1)
+    ax.axonn_fc_forward(h, I, What, O)
+    ax.axonn_fc_backward(h, dO, dI, dW)
+    ax.axonn_grads_sync()
+    torch.cuda.synchronize()
+    ax.axonn_fc_destroy(h)
+    return (X, W, dY), (O, dI, dW.reshape(k, n))
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+@pytest.mark.parametrize("m,k,n", [(256, 512, 1024), (384, 200, 136)])
+def test_integer_bit_exact(ax, m, k, n, transposed):
+    torch = require_cuda()
+    (X, W, dY), outs = _layer(ax, m, k, n, transposed, "int", torch.bfloat16)
+    for got, ref in zip(outs, fc.fc_layer(X, W, dY)):
+        want = synthdata.bf16_bits(synthdata.bf16_round(ref))
+        assert np.array_equal(bf16_bits_of(got), want)
+
+
+@pytest.mark.parametrize("m,k,n", [(256, 512, 1024), (2048, 1024, 3072)])
+def test_random_within_tolerance(ax, m, k, n):
+    torch = require_cuda()
+    (X, W, dY), outs = _layer(ax, m, k, n, False, "uniform", torch.bfloat16)
+    for got, ref in zip(outs, fc.fc_layer(X, W, dY)):
+        assert normwise_err(to_host_f64(got), ref) <= 2e-2
+
+
+def test_f32_mode_bit_exact(ax):
+    torch = require_cuda()
+    (X, W, dY), outs = _layer(ax, 192, 96, 160, False, "int", torch.float32)
+    for got, ref in zip(outs, fc.fc_layer(X, W, dY)):
+        np.testing.assert_array_equal(to_host_f64(got), ref)
+
+
+def test_backward_before_forward_is_state_error(ax):
+    torch = require_cuda()
+    h = ax.axonn_fc_create(128, 128, 128)
+    t = torch.zeros((128, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_fc_backward(h, t, t, t)
+    assert e.value.status == ax.AXONN_ERR_STATE
+    ax.axonn_fc_destroy(h)
+
+
+def test_kernel_launch_counter_and_profile(ax):
+    torch = require_cuda()
+    n0 = ax.axonn_kernel_launches()
+    ax.axonn_profile_enable(True)
+    _layer(ax, 256, 256, 256, False, "uniform", torch.bfloat16)
+    ax.axonn_profile_enable(False)
+    launches, ms, flops = ax.axonn_profile_read()
+    assert ax.axonn_kernel_launches() - n0 == 3 == launches
+    assert flops == 3 * 2 * 256 ** 3 and ms > 0

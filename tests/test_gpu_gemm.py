@@ -1,0 +1,145 @@
+"""Parity of the three local products (Alg. 1 lines 3, 11, 13) through the C ABI
+(axonn_gemm) against the fp64 oracle (oracle.fc).
+
+  * integer inputs in [-4, 4]: every partial sum is an exact integer < 2^24, so
+    the tcgen05 result must equal RNE_bf16(exact) bit for bit — catches any
+    tile, swizzle, descriptor or indexing bug;
+  * uniform(-1,1) bf16 inputs: normwise error <= 2e-2 (BASELINE.json
+    north_star);
+  * fp32 test mode (SIMT): bit-exact on integers, <= 1e-5 on random inputs.
+Shapes span several 128x256 tiles, ragged tails in M, N and K, strided rows and
+the degenerate K == 0 and M == 0 cases."""
+import numpy as np
+import pytest
+
+import synthdata
+from oracle import fc
+from gpu_util import (bf16_bits_of, empty_dev, normwise_err, require_cuda, round_up, to_dev,
+                      to_host_f64)
+
+pytestmark = pytest.mark.gpu
+
+OPS = {"NN": 0, "NT": 1, "TN": 2}
+
+
+def _operands(op, M, N, K, kind, seed=42):
+    # storage layouts of A and B for each op (include/axonn.h)
+    a_shape = (K, M) if op == "TN" else (M, K)
+    b_shape = (N, K) if op == "NT" else (K, N)
+    A = synthdata.tensor(a_shape, 1000 + M, seed, kind)
+    B = synthdata.tensor(b_shape, 2000 + N, seed, kind)
+    return A, B
+
+
+def _oracle(op, A, B):
+    if op == "NN":
+        return fc.fc_forward(A, B)             # I x W
+    if op == "NT":
+        return fc.fc_backward_input(A, B)      # dO x W^T
+    return fc.fc_backward_weight(A, B)         # I^T x dO
+
+
+def _run(op, A, B, M, N, dtype, pad=0):
+    torch = require_cuda()
+    import paper_2502_08145_b200 as ax
+    lda = round_up(A.shape[1]) + pad
+    ldb = round_up(B.shape[1]) + pad
+    ldc = round_up(N) + pad
+    dA = to_dev(A, dtype, lda)
+    dB = to_dev(B, dtype, ldb)
+    dC = empty_dev(M, N, dtype, ldc)
+    K = A.shape[0] if op == "TN" else A.shape[1]
+    ax.axonn_gemm(OPS[op], ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16,
+                  M, N, K, dA, lda, dB, ldb, dC, ldc)
+    torch.cuda.synchronize()
+    return dC
+
+
+SHAPES = [(128, 256, 64), (256, 512, 128), (384, 768, 320), (300, 520, 200), (257, 129, 65),
+          (1, 8, 8), (129, 257, 1000), (1024, 1024, 1024), (640, 2304, 96)]
+
+
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_bf16_integer_bit_exact(op, M, N, K):
+    torch = require_cuda()
+    A, B = _operands(op, M, N, K, "int")
+    ref = _oracle(op, A, B)
+    want = synthdata.bf16_bits(synthdata.bf16_round(ref))
+    got = bf16_bits_of(_run(op, A, B, M, N, torch.bfloat16))
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, f"{len(bad)} mismatches, first at {bad[:3].tolist()}"
+
+
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("M,N,K", [(384, 768, 320), (300, 520, 200), (2048, 1536, 1024)])
+def test_bf16_random_within_tolerance(op, M, N, K):
+    torch = require_cuda()
+    A, B = _operands(op, M, N, K, "uniform")
+    ref = _oracle(op, A, B)
+    got = to_host_f64(_run(op, A, B, M, N, torch.bfloat16, pad=8))
+    assert normwise_err(got, ref) <= 2e-2
+    # one bf16 rounding of an fp32 sum: per element within 2^-8 relative + accumulation slack
+    assert np.all(np.abs(got - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-5 * np.sqrt(K))
+
+
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("M,N,K", [(300, 520, 200), (257, 129, 65), (64, 64, 1)])
+def test_f32_mode(op, M, N, K):
+    torch = require_cuda()
+    A, B = _operands(op, M, N, K, "int")
+    got = to_host_f64(_run(op, A, B, M, N, torch.float32))
+    np.testing.assert_array_equal(got, _oracle(op, A, B))
+    A, B = _operands(op, M, N, K, "uniform")
+    ref = _oracle(op, A, B)
+    assert normwise_err(to_host_f64(_run(op, A, B, M, N, torch.float32)), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("op", list(OPS))
+def test_k_zero_writes_zeros_and_m_zero_is_noop(op):
+    torch = require_cuda()
+    import paper_2502_08145_b200 as ax
+    C = torch.full((16, 24), 7.0, dtype=torch.bfloat16, device="cuda")
+    A = torch.zeros((16, 8), dtype=torch.bfloat16, device="cuda")
+    ax.axonn_gemm(OPS[op], ax.AXONN_BF16, 16, 24, 0, A, 8, A, 8, C, 24)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(C).item() == 0
+    ax.axonn_gemm(OPS[op], ax.AXONN_BF16, 0, 24, 8, A, 8, A, 24, C, 24)
+
+
+def test_deterministic():
+    torch = require_cuda()
+    A, B = _operands("TN", 1024, 1024, 2048, "uniform")
+    c1 = bf16_bits_of(_run("TN", A, B, 1024, 1024, torch.bfloat16))
+    c2 = bf16_bits_of(_run("TN", A, B, 1024, 1024, torch.bfloat16))
+    assert np.array_equal(c1, c2)
+
+
+def test_bad_alignment_is_an_error():
+    torch = require_cuda()
+    import paper_2502_08145_b200 as ax
+    A = torch.zeros((64, 66), dtype=torch.bfloat16, device="cuda")
+    C = torch.zeros((64, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_gemm(0, ax.AXONN_BF16, 64, 64, 60, A, 66, A, 66, C, 64)
+    assert e.value.status == ax.AXONN_ERR_ARG
+
+
+@pytest.mark.parametrize("op,M,N,K", [("NN", 16384, 12288, 4096),   # C2 QKV forward
+                                      ("NT", 16384, 4096, 16384),   # C2 fc2 backward dI
+                                      ("TN", 16384, 4096, 16384)])  # C2 fc2 dW (M=4h rows)
+def test_full_size_sampled(op, M, N, K):
+    """BASELINE.json C2 shapes in the launch configuration bench.py times; 4096
+    sampled entries each checked against an exact fp64 dot product."""
+    torch = require_cuda()
+    A, B = _operands(op, M, N, K, "uniform")
+    C = _run(op, A, B, M, N, torch.bfloat16)
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, M, 4096)
+    cols = rng.integers(0, N, 4096)
+    AA = A.T if op == "TN" else A
+    BB = B.T if op == "NT" else B
+    ref = fc.dot_entries(AA, BB, rows, cols)
+    got = C[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()].double().cpu().numpy()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 2e-2
+    assert np.all(np.abs(got - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-5 * np.sqrt(K))
