@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the 3D-PMM FC hot path (AxoNN, arXiv 2502.08145) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--grid gx,gy,gz,gd] [--model 5B|10B|20B|40B|80B] [--tokens-per-gpu T]
+
+A "step" is one pass of the whole hot path over one batch: Alg. 1 forward of
+the four FC layers of one GPT block (QKV h->3h, proj h->h, fc1 h->4h, fc2
+4h->h; Table II shapes; proj and fc2 transposed,
+PAPER.md:402-414), then their backward in reverse order, then the ORS /
+data-parallel wait point (axonn_grads_sync).
+
+N = 1: BASELINE.json configs[1] (C2): GPT-5B block, m = 16,384 tokens, grid
+1x1x1x1.  N > 1: the same block weak-scaled (16,384 tokens per GPU, global
+m = 16,384 N) on the grid the paper's performance model ranks first
+(axonn_grid_select, uniform NVSwitch bandwidth), unless --grid is given.
+
+value = model flops of the step (6 m k n per layer, PAPER.md:786-795,
+SPEC.md:443) summed over ranks / device time of the step (CUDA events on the
+launching stream, max over ranks), in TFLOP/s.  e2e = the same metric with the
+per-step inputs (I and dO of every layer) copied host->device from pinned
+memory and the weight gradients read back, inside the timed region.
+--impl reference times the CPU fp64 oracle (oracle/) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "bf16 TFLOP/s per GPU (fraction of peak) for 3D-PMM FC fwd+bwd at 1/2/4/8 B200"
+HIDDEN = {"5B": 4096, "10B": 5120, "20B": 7168, "40B": 9216, "80B": 12288}
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+
+
+def block_layers(h: int, m: int):
+    """(m, k, n, transposed) of the four FC layers of one GPT block, phase A (R2b)."""
+    return [(m, h, 3 * h, False), (m, h, h, True), (m, h, 4 * h, False), (m, 4 * h, h, True)]
+
+
+def model_flops(layers) -> float:
+    return float(sum(6 * m * k * n for m, k, n, _ in layers))
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during timing."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for _, _, r in rows for n, v in zip(names, r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(h: int, m_sample: int, min_seconds: float):
+    """Time the fp64 oracle (oracle.fc) on the block's layers with m_sample rows,
+    repeating until min_seconds elapsed.  Returns (TFLOP/s, threads, description)."""
+    import numpy as np
+    from oracle import fc
+    import synthdata
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # pragma: no cover
+        threads = os.cpu_count()
+    layers = block_layers(h, m_sample)
+    data = [synthdata.layer_tensors(m, k, n, i) for i, (m, k, n, _) in enumerate(layers)]
+    data = [tuple(a.astype(np.float64) for a in d) for d in data]
+    flops, t0, reps = 0.0, time.perf_counter(), 0
+    while True:
+        for (X, W, dY), L in zip(data, layers):
+            fc.fc_layer(X, W, dY)
+            flops += model_flops([L])
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or reps >= 50:
+            break
+    desc = (f"oracle.fc fp64 (numpy BLAS) on the GPT block's 4 FC layers fwd+bwd with "
+            f"{m_sample} of the workload's token rows (h={h}), {reps} rep(s), {el:.1f} s")
+    return flops / el / 1e12, threads, desc
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.gpus
+    h = HIDDEN[args.model]
+    m_ref = 256
+    import numpy as np
+    from oracle import fc
+    import synthdata
+    layers = block_layers(h, m_ref)
+    data = [tuple(a.astype(np.float64) for a in synthdata.layer_tensors(m, k, nn, i))
+            for i, (m, k, nn, _) in enumerate(layers)]
+    def step():
+        for X, W, dY in data:
+            fc.fc_layer(X, W, dY)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    val = model_flops(layers) * args.steps / el / 1e12
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # pragma: no cover
+        threads = os.cpu_count()
+    sample = (f"oracle.fc fp64 on the GPT-{args.model} block's 4 FC layers fwd+bwd, {m_ref} token "
+              f"rows per step (bounded sample of the {16384 * n}-token workload)")
+    out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": n,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": workload_config(args.model, n, None),
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(model, n, grid):
+    h = HIDDEN[model]
+    return {"workload": (f"GPT-{model} block FC layers (QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h; "
+                         f"h={h}) Alg. 1 fwd+bwd, 16384 tokens per GPU"
+                         + (" (BASELINE.json configs[1], C2)" if n == 1 and model == "5B" else
+                            f", global m={16384 * n}")),
+            "grid": list(grid) if grid else None, "tokens": 16384 * n, "hidden": h,
+            "phase": "A (proj, fc2 transposed)",
+            "l2": "no flush: per-step operands (>= 134 MB each for I/dO of the fc2 layer) exceed the 126 MB L2"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="axonn", choices=["axonn", "reference"])
+    ap.add_argument("--grid", default=None, help="gx,gy,gz,gd (default: model-selected)")
+    ap.add_argument("--model", default="5B", choices=sorted(HIDDEN))
+    ap.add_argument("--chunks", type=int, default=4, help="forward AR pipelining chunks")
+    ap.add_argument("--gemm-sms", type=int, default=0, help="SM budget of the GEMM grid (0 = all)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2502_08145_b200 as ax
+
+    h = HIDDEN[args.model]
+    m = 16384 * world
+    layers = block_layers(h, m)
+    if args.grid:
+        grid = tuple(int(x) for x in args.grid.split(","))
+    elif world == 1:
+        grid = (1, 1, 1, 1)
+    else:
+        tb = {(g0, g1): 1.0e11 for g0 in range(1, 9) for g1 in range(2, 9) if g0 * g1 <= 8}
+        best = ax.axonn_grid_select(layers, world, 8, tb, 1.0e11, 2, 0, cap=1)[0]
+        grid = (best["gx"], best["gy"], best["gz"], best["gd"])
+
+    if world > 1:
+        ax.bootstrap_from_torch_distributed(local)
+    ax.axonn_grid_init(*grid)
+    if args.gemm_sms:
+        ax.axonn_set_gemm_sms(args.gemm_sms)
+
+    stream = torch.cuda.Stream()
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(42 + rank)
+    bf = torch.bfloat16
+
+    def rnd(*shape):
+        t = torch.empty(shape, dtype=torch.float32, device="cuda")
+        t.uniform_(-1.0, 1.0, generator=gen)
+        return t.to(bf)
+
+    L = []
+    for (mm, k, n, t) in layers:
+        hd = ax.axonn_fc_create(mm, k, n, t, ax.AXONN_BF16, args.chunks)
+        g = ax.axonn_fc_geometry(hd)
+        L.append({"h": hd, "g": g, "I": rnd(g.m_l, g.k_l), "W": rnd(g.what_len),
+                  "O": torch.empty(g.m_l, g.n_l, dtype=bf, device="cuda"),
+                  "dO": rnd(g.m_l, g.n_l), "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
+                  "dW": torch.empty(g.what_len, dtype=bf, device="cuda")})
+
+    def step(s):
+        for i, l in enumerate(L):
+            ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
+            if i + 1 < len(L):  # OAG: prefetch the next layer's all-gather
+                ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], s)
+        for l in reversed(L):
+            ax.axonn_fc_backward(l["h"], l["dO"], l["dI"], l["dW"], s)
+        ax.axonn_grads_sync(s)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(stream)
+    barrier()
+
+    # ---------------------------------------------------------------- timed region
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ax.axonn_kernel_launches()
+    ax.axonn_profile_read()
+    ax.axonn_profile_enable(True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                step(stream)
+        ev1.record(stream)
+        barrier()
+    ax.axonn_profile_enable(False)
+    launches = ax.axonn_kernel_launches() - launches0
+    gemm_n, gemm_ms, gemm_flops = ax.axonn_profile_read()
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    flops_step = model_flops(layers)              # whole job (all ranks)
+    value = flops_step / (t_ms * 1e-3) / 1e12
+
+    peaks, peaks_src = read_peaks()
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    peak = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
+    burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        hI = [l["I"].cpu().pin_memory() for l in L]
+        hdO = [l["dO"].cpu().pin_memory() for l in L]
+        hdW = [torch.empty(l["dW"].shape, dtype=bf).pin_memory() for l in L]
+        copy = torch.cuda.Stream()
+        evI = [torch.cuda.Event() for _ in L]
+        evO = [torch.cuda.Event() for _ in L]
+        bi = sum(t.numel() * 2 for t in hI + hdO)
+        bo = sum(t.numel() * 2 for t in hdW)
+
+        def e2e_step():
+            # H2D on a copy stream in the order the step consumes them
+            with torch.cuda.stream(copy):
+                copy.wait_stream(stream)
+                for i, l in enumerate(L):
+                    l["I"].copy_(hI[i], non_blocking=True)
+                    evI[i].record(copy)
+                for i in reversed(range(len(L))):
+                    L[i]["dO"].copy_(hdO[i], non_blocking=True)
+                    evO[i].record(copy)
+            with torch.cuda.stream(stream):
+                for i, l in enumerate(L):
+                    stream.wait_event(evI[i])
+                    ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], stream)
+                    if i + 1 < len(L):
+                        ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
+                for i in reversed(range(len(L))):
+                    stream.wait_event(evO[i])
+                    ax.axonn_fc_backward(L[i]["h"], L[i]["dO"], L[i]["dI"], L[i]["dW"], stream)
+                ax.axonn_grads_sync(stream)
+                for i, l in enumerate(L):
+                    hdW[i].copy_(l["dW"], non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ksteps = max(3, min(args.steps, 10))
+        barrier()
+        e0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        te = max_over_ranks(e0.elapsed_time(e1)) / ksteps
+        e2e = {"value": flops_step / (te * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world,
+               "ms_per_step": te, "steps": ksteps,
+               "path": "pinned host -> device copies on a side stream + axonn_fc_forward/backward"
+                       " + grads_sync + dW device->host, all inside the timed region"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, thr, desc = oracle_sample(h, 2048, 10.0)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (uniform(-1,1) bf16, device-generated, seeded)",
+            "config": workload_config(args.model, world, grid),
+            "per_gpu_tflops": value / world,
+            "frac_of_peak": {"advertised_2250": value / world / 2250.0,
+                             "measured_burst": value / world / burst,
+                             "measured_sustained": value / world / peak, "peaks": peaks_src},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "traffic": traffic,
+                         "kernel": "gemm_bf16_tcgen05 (all NN/NT/TN launches of the timed region;"
+                                   " achieved = sum 2MNK / sum event time)",
+                         "peak_kind": f"bf16_tflops_sustained, {peaks_src}",
+                         "frac_of_burst": achieved / burst if burst else None,
+                         "gemm_launches": gemm_n, "gemm_ms_per_step": gemm_ms / args.steps},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    ax.axonn_grid_finalize()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
