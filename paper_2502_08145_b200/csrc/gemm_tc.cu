@@ -23,6 +23,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "gemm.h"
 #include "ptx.cuh"
@@ -55,6 +57,17 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n)
   const int gm = min(tiles_m - first_m, GROUP_M);
   const int r = t - g * per_group;
   return {(first_m + r % gm) * BM, (r / gm) * BN};
+}
+
+
+__device__ __forceinline__ TileCoord tile_coord_g(int t, int tiles_m, int tiles_n, int group_m,
+                                                  int bm, int bn) {
+  const int per_group = group_m * tiles_n;
+  const int g = t / per_group;
+  const int first_m = g * group_m;
+  const int gm = min(tiles_m - first_m, group_m);
+  const int r = t - g * per_group;
+  return {(first_m + r % gm) * bm, (r / gm) * bn};
 }
 
 // A_MN / B_MN: 0 = operand stored K-major in HBM, 1 = stored MN-major.
@@ -225,6 +238,194 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
+
+// ===================================================================== 2-CTA
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256x256 tile.  Each CTA stages 128 rows of A and 128 rows (N) of B per
+// 64-wide K block (32 KiB per stage, 6 stages); the leader CTA issues
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads the peer's half
+// of A and B through the pair's shared operand path; each CTA's TMEM holds its
+// 128 rows of the fp32 accumulator (two 256-column buffers = all 512 columns).
+// Per tile and K block the pair moves 64 KiB from L2 instead of the 96 KiB two
+// independent 128x256 CTAs need.
+constexpr int P_BM = 256;                 // tile rows per pair (128 per CTA)
+constexpr int P_BN = 256;
+constexpr int P_STAGES = 6;
+constexpr int P_SMEM_A = 128 * BK * 2;    // 16 KiB per CTA
+constexpr int P_SMEM_B = 128 * BK * 2;    // 16 KiB per CTA (half of N)
+constexpr int P_STAGE_BYTES = P_SMEM_A + P_SMEM_B;
+constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + 256;
+
+template <int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB,
+                           __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
+                           int group_m) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P_STAGES * P_SMEM_A;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_SMEM_B);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int tiles_m = (M + P_BM - 1) / P_BM;
+  const int tiles_n = (N + P_BN - 1) / P_BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < P_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, P_BM, P_BN);
+        const int am = tc.m0 + 128 * static_cast<int>(rank);   // this CTA's A rows
+        const int bn = tc.n0 + 128 * static_cast<int>(rank);   // this CTA's half of N
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* a_dst = sA + stage * P_SMEM_A;
+          uint8_t* b_dst = sB + stage * P_SMEM_B;
+          if (A_MN == 0) {
+            ptx::tma_load_2d_2sm(a_dst, &tmA, &full[stage], k0, am);
+          } else {
+            ptx::tma_load_2d_2sm(a_dst, &tmA, &full[stage], am, k0);
+            ptx::tma_load_2d_2sm(a_dst + MN_CHUNK_BYTES, &tmA, &full[stage], am + MN_CHUNK, k0);
+          }
+          if (B_MN == 0) {
+            ptx::tma_load_2d_2sm(b_dst, &tmB, &full[stage], k0, bn);
+          } else {
+            ptx::tma_load_2d_2sm(b_dst, &tmB, &full[stage], bn, k0);
+            ptx::tma_load_2d_2sm(b_dst + MN_CHUNK_BYTES, &tmB, &full[stage], bn + MN_CHUNK, k0);
+          }
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(P_BM, P_BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * P_BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sA + stage * P_SMEM_A);
+          const uint32_t b_base = ptx::smem_u32(sB + stage * P_SMEM_B);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_base + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                     : ptx::sdesc_sw128(a_base + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                     : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
+            ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          ptx::umma_commit_2sm(&empty[stage], 0x3);  // frees the slot in both CTAs
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit_2sm(&tfull[acc], 0x3);      // both halves of the accumulator ready
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (both CTAs)
+    const int e = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, P_BM, P_BN);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = tc.m0 + 128 * static_cast<int>(rank) + 32 * e + lane;
+      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll 1
+      for (int c = 0; c < P_BN / 32; ++c) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) +
+                               static_cast<uint32_t>(acc * P_BN + c * 32);
+        ptx::tmem_ld_32x32b_x32(taddr, v);
+        ptx::tmem_wait_ld();
+        const int col0 = tc.n0 + c * 32;
+        if (row < M && col0 < N) {
+          if (vec_ok && col0 + 32 <= N) {
+            uint4* dst = reinterpret_cast<uint4*>(crow + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 w;
+              w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+              w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+              w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+              w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+              dst[q] = w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (col0 + q < N) crow[col0 + q] = __float2bfloat16_rn(__uint_as_float(v[q]));
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -257,8 +458,8 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
 }
 
 template <int A_MN, int B_MN>
-cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M,
-                   int N, int K, int num_sms, cudaStream_t stream) {
+cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
+                          int M, int N, int K, int num_sms, cudaStream_t stream) {
   auto kern = gemm_bf16_tcgen05<A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -274,9 +475,36 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_
   return cudaGetLastError();
 }
 
+template <int A_MN, int B_MN>
+cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
+                        int M, int N, int K, int num_sms, int group_m, cudaStream_t stream) {
+  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(P_SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + P_BM - 1) / P_BM) * ((N + P_BN - 1) / P_BN);
+  int grid = (num_sms / 2) * 2;
+  if (2 * tiles < grid) grid = 2 * tiles;
+  if (grid < 2) grid = 2;
+  kern<<<grid, THREADS, P_SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
+                                                N, K, group_m);
+  return cudaGetLastError();
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 }  // namespace
 
 // C[M][N] (bf16, ldc) = op(A) x op(B); see axonn_gemm in include/axonn.h.
+// AXONN_GEMM_VARIANT=single selects the 1-CTA kernel (kept for A/B timing);
+// the default is the CTA-pair kernel.  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
                         cudaStream_t stream) {
@@ -284,28 +512,39 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if ((lda & 7) || (ldb & 7) || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
     return GemmStatus::kBadAlignment;
+  static const bool single = [] {
+    const char* v = std::getenv("AXONN_GEMM_VARIANT");
+    return v && std::strcmp(v, "single") == 0;
+  }();
+  static const int group_m = env_int("AXONN_GROUP_M", 16);
   CUtensorMap ma, mb;
-  bool ok = true;
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
-  cudaError_t e = cudaSuccess;
+  // B box rows along N: 256 for the single-CTA tile, 128 (half of N) per CTA of a pair.
+  const uint32_t bkrows = single ? BN : 128;
+  bool ok;
   switch (op) {
-    case 0:  // NN: A [M][K], B [K][N]
-      ok = make_map(&ma, A, K, M, lda, BK, BM) && make_map(&mb, B, N, K, ldb, MN_CHUNK, BK);
-      if (!ok) return GemmStatus::kTensorMap;
-      e = launch<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
+    case 0:  // NN: A [M][K] (K-major), B [K][N] (N-major)
+      ok = make_map(&ma, A, K, M, lda, BK, 128) && make_map(&mb, B, N, K, ldb, MN_CHUNK, BK);
       break;
-    case 1:  // NT: A [M][K], B [N][K]
-      ok = make_map(&ma, A, K, M, lda, BK, BM) && make_map(&mb, B, K, N, ldb, BK, BN);
-      if (!ok) return GemmStatus::kTensorMap;
-      e = launch<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream);
+    case 1:  // NT: A [M][K], B [N][K] (K-major)
+      ok = make_map(&ma, A, K, M, lda, BK, 128) && make_map(&mb, B, K, N, ldb, BK, bkrows);
       break;
-    case 2:  // TN: A [K][M], B [K][N]
+    case 2:  // TN: A [K][M] (M-major), B [K][N]
       ok = make_map(&ma, A, M, K, lda, MN_CHUNK, BK) && make_map(&mb, B, N, K, ldb, MN_CHUNK, BK);
-      if (!ok) return GemmStatus::kTensorMap;
-      e = launch<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
       break;
     default:
       return GemmStatus::kBadOp;
+  }
+  if (!ok) return GemmStatus::kTensorMap;
+  cudaError_t e;
+  if (single) {
+    e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
+        : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
+                  : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
+  } else {
+    e = op == 0 ? launch_pair<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, stream)
+        : op == 1 ? launch_pair<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, group_m, stream)
+                  : launch_pair<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, stream);
   }
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
 }
