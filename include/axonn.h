@@ -206,6 +206,12 @@ int64_t axonn_kernel_launches(void);
 /* SM budget of the persistent GEMM grid (<= 0 or > #SMs: all SMs).  Leaving
  * SMs free lets NCCL kernels run beside the GEMM when collectives overlap. */
 axonn_status_t axonn_set_gemm_sms(int sms);
+/* Bytes this rank sends in ring collectives issued since the last reset,
+ * computed from the element counts passed to NCCL with the ring formulas of
+ * Eqs. 1-5 (all-gather (p-1)*count*b, reduce-scatter (p-1)*recvcount*b,
+ * all-reduce 2(p-1)/p*count*b): out = {AG_z, RS_z, forward AR (Eq. 3 form),
+ * backward dI AR (Eq. 4 form), data-parallel AR (Eq. 5)} (host). */
+axonn_status_t axonn_comm_bytes(int64_t out[5], int reset);
 
 /* ======================================================================== */
 /* Performance model: Eqs. 1-6 per layer, summed over     */

@@ -4,7 +4,7 @@ Every function here has the name of the C entry point it calls and does no
 arithmetic of the method: shapes, pointers and streams are passed through
 ctypes; every step of the hot path runs in the library's CUDA kernels and
 NCCL calls.  Importing this module fails loudly if the library has not been
-built (``python -m paper_2502_08145_b200.build``); there is no fallback.
+built (``python paper_2502_08145_b200/build.py``); there is no fallback.
 
 torch is used only for device memory, streams and torch.distributed
 bootstrap, and is imported lazily so the pure-host calls work without it.
@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libaxonn.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2502_08145_b200.build`")
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2502_08145_b200/build.py`")
 _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
 
 # ---------------------------------------------------------------- constants
@@ -94,6 +94,7 @@ _PROTOS = {
     "axonn_profile_read": (_S, [POINTER(c_int64), POINTER(c_double), POINTER(c_double)]),
     "axonn_kernel_launches": (c_int64, []),
     "axonn_set_gemm_sms": (_S, [c_int]),
+    "axonn_comm_bytes": (_S, [POINTER(c_int64), c_int]),
     "axonn_grid_select": (_S, [POINTER(LayerT), c_int, c_int, c_int, POINTER(BwEntry), c_int,
                                c_double, c_int, c_int, POINTER(GridScore), c_int, POINTER(c_int)]),
 }
@@ -243,6 +244,12 @@ def axonn_kernel_launches() -> int:
 
 def axonn_set_gemm_sms(sms: int) -> None:
     _check(_lib.axonn_set_gemm_sms(sms))
+
+
+def axonn_comm_bytes(reset: bool = False) -> dict:
+    out = (c_int64 * 5)()
+    _check(_lib.axonn_comm_bytes(out, int(bool(reset))))
+    return dict(zip(("ag_z", "rs_z", "ar_fwd", "ar_bwd", "ar_d"), list(out)))
 
 
 def axonn_grid_select(layers, G, g_node, table, beta_inter, bytes_per_elem=2, fixed_gd=0,

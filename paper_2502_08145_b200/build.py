@@ -1,6 +1,6 @@
 """Build libaxonn.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2502_08145_b200.build
+    python paper_2502_08145_b200/build.py      (or __graft_entry__.build())
 
 Objects go to paper_2502_08145_b200/build/, the library to
 paper_2502_08145_b200/libaxonn.so (git-ignored, travels with gpurun).

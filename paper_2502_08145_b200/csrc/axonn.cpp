@@ -89,6 +89,7 @@ struct State {
   std::vector<cudaEvent_t> pending_grads;
   std::set<struct ::axonn_fc*> handles;
   bool profiling = false;
+  int64_t comm_bytes[5] = {0, 0, 0, 0, 0};  // ring bytes sent per rank: ag_z, rs_z, ar_fwd, ar_bwd, ar_d
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_free;
 };
@@ -119,6 +120,19 @@ axonn_status_t ensure_device() {
   S.num_sms = sms;
   if (S.gemm_sms <= 0 || S.gemm_sms > sms) S.gemm_sms = sms;
   return AXONN_OK;
+}
+
+
+// Per-rank bytes a ring collective sends (Assumption-1):
+// all-gather (p-1)*count, reduce-scatter (p-1)*recvcount, all-reduce
+// 2(p-1)/p*count — the quantities of Eqs. 1-5.
+void count_comm(int kind, int p, size_t count, int dtype) {
+  const int64_t b = static_cast<int64_t>(elem_size(dtype));
+  const int64_t c = static_cast<int64_t>(count);
+  int64_t bytes = 0;
+  if (kind == 0 || kind == 1) bytes = (p - 1) * c * b;           // AG: count = sendcount; RS: recvcount
+  else bytes = (2 * (p - 1) * c * b) / p;                         // AR
+  S.comm_bytes[kind] += bytes;
 }
 
 axonn_status_t check_async_nccl() {
@@ -268,6 +282,7 @@ axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) 
   CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_in, 0));
   NCCL_TRY(ncclAllGather(W_hat, h->wbuf, S_el, nccl_type(h->d.dtype), S.axis_comm[AX_Z],
                          S.cstream[AX_Z]));
+  count_comm(0, S.g[AX_Z], S_el, h->d.dtype);
   CUDA_TRY(cudaEventRecord(h->ev_ag, S.cstream[AX_Z]));
   h->prefetched = true;
   return AXONN_OK;
@@ -493,6 +508,7 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
       CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
       NCCL_TRY(ncclAllReduce(Oc, Oc, static_cast<size_t>(rows * g.n_l), nccl_type(h->d.dtype),
                              ncclSum, S.axis_comm[h->ax_fwd], cs));
+      count_comm(2, P, static_cast<size_t>(rows * g.n_l), h->d.dtype);
     }
     if (g.m_l == 0) break;
   }
@@ -529,8 +545,9 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   if (Pb > 1) {
     CUDA_TRY(cudaEventRecord(h->ev_dw, st));
     CUDA_TRY(cudaStreamWaitEvent(bs, h->ev_dw, 0));
-    NCCL_TRY(ncclAllReduce(dI_local, dI_local, static_cast<size_t>((g.m_l * g.k_l) != 0), nt, ncclSum,
+    NCCL_TRY(ncclAllReduce(dI_local, dI_local, static_cast<size_t>(g.m_l * g.k_l), nt, ncclSum,
                            S.axis_comm[h->ax_bwd], bs));
+    count_comm(3, Pb, static_cast<size_t>(g.m_l * g.k_l), dt);
     CUDA_TRY(cudaEventRecord(h->ev_ar, bs));
   }
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
@@ -539,13 +556,14 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   STATUS_TRY(run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst,
                       g.n_l, st));
   // line 14: dW_hat = reduce-scatter_z(dW partial)   (ORS: waited in grads_sync)
-  const size_t S_el = static_cast<size_t>(g.what_len != 0);
+  const size_t S_el = static_cast<size_t>(g.what_len);
   cudaEvent_t last = nullptr;
   if (rs) {
     CUDA_TRY(cudaEventRecord(h->ev_rs, st));
     CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
     NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_Z],
                                S.cstream[AX_Z]));
+    count_comm(1, S.g[AX_Z], S_el, dt);
     CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_Z]));
     last = h->ev_grad;
   }
@@ -555,6 +573,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_D], h->ev_rs, 0));
     NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_D],
                            S.cstream[AX_D]));
+    count_comm(4, S.g[AX_D], S_el, dt);
     CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_D]));
     last = h->ev_grad;
   }
@@ -639,6 +658,16 @@ axonn_status_t axonn_profile_read(int64_t* launches, double* ms, double* flops) 
 }
 
 int64_t axonn_kernel_launches(void) { return g_launches.load(); }
+
+axonn_status_t axonn_comm_bytes(int64_t out[5], int reset) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!out) return fail(AXONN_ERR_ARG, "NULL argument");
+  for (int i = 0; i < 5; ++i) {
+    out[i] = S.comm_bytes[i];
+    if (reset) S.comm_bytes[i] = 0;
+  }
+  return AXONN_OK;
+}
 
 axonn_status_t axonn_set_gemm_sms(int sms) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
