@@ -50,6 +50,17 @@ def model_flops(layers) -> float:
     return float(sum(6 * m * k * n for m, k, n, _ in layers))
 
 
+def reduce_max(x: float, device: str = "cuda") -> float:
+    """Max of a per-rank float over all ranks (device timing is max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def read_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -271,11 +282,7 @@ def main():
             torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(x, "cuda")
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
