@@ -284,6 +284,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         return reduce_max(x, "cuda")
 
+    ax.axonn_comm_bytes(reset=True)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step(stream)
@@ -304,6 +305,7 @@ def main():
         barrier()
     ax.axonn_profile_enable(False)
     launches = ax.axonn_kernel_launches() - launches0
+    comm0 = ax.axonn_comm_bytes(reset=True)
     gemm_n, gemm_ms, gemm_flops = ax.axonn_profile_read()
     t_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     flops_step = model_flops(layers)              # whole job (all ranks)
@@ -370,6 +372,37 @@ def main():
                "path": "pinned host -> device copies on a side stream + axonn_fc_forward/backward"
                        " + grads_sync + dW device->host, all inside the timed region"}
 
+    # ---------------------------------------------------------------- GEMM-only (exposed comm)
+    exposed = None
+    if world > 1:
+        scratch = []
+        for l in L:
+            g = l["g"]
+            scratch.append((g, torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda").uniform_(-1, 1),
+                            torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda")))
+
+        def gemm_step(s):
+            for l, (g, Wf, _) in zip(L, scratch):
+                ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, s)
+            for l, (g, Wf, dWf) in zip(reversed(L), reversed(scratch)):
+                ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, s)
+                ax.axonn_gemm(2, 0, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, s)
+
+        for _ in range(2):
+            gemm_step(stream)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            gemm_step(stream)
+        g1.record(stream)
+        barrier()
+        t_gemm = max_over_ranks(g0.elapsed_time(g1)) / args.steps
+        exposed = {"t_step_ms": t_ms, "t_gemm_only_ms": t_gemm,
+                   "exposed_comm_frac": max(0.0, (t_ms - t_gemm) / t_ms),
+                   "comm_bytes_per_rank_per_step": {k: v // max(1, args.steps + args.warmup)
+                                                    for k, v in comm0.items()}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, thr, desc = oracle_sample(h, 2048, 10.0)
@@ -395,6 +428,7 @@ def main():
                          "frac_of_burst": achieved / burst if burst else None,
                          "gemm_launches": gemm_n, "gemm_ms_per_step": gemm_ms / args.steps},
             "gpu_launches": launches,
+            "overlap": exposed,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
