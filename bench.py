@@ -50,6 +50,15 @@ def model_flops(layers) -> float:
     return float(sum(6 * m * k * n for m, k, n, _ in layers))
 
 
+_JSON_OUT = None
+
+
+def emit(obj) -> None:
+    f = _JSON_OUT or sys.stdout
+    f.write(json.dumps(obj) + "\n")
+    f.flush()
+
+
 def reduce_max(x: float, device: str = "cuda") -> float:
     """Max of a per-rank float over all ranks (device timing is max over ranks)."""
     import torch
@@ -185,7 +194,7 @@ def run_reference(args):
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def workload_config(model, n, grid):
@@ -213,6 +222,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    # Exactly one JSON line on stdout: libraries (NCCL prints its version line)
+    # write to fd 1, so fd 1 is pointed at stderr and the JSON goes to a copy.
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(out_fd, "w")
     if args.impl == "reference":
         run_reference(args)
         return
@@ -433,7 +448,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     ax.axonn_grid_finalize()
     if world > 1:
         dist.destroy_process_group()

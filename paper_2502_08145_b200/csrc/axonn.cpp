@@ -536,46 +536,61 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   cudaStream_t st = as_stream(stream);
   const int dt = h->d.dtype;
   const ncclDataType_t nt = nccl_type(dt);
-  // line 11: dI^ = dO x W^T       (M = m_l, N = k_l, K = n_l)
-  STATUS_TRY(run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
-                      dI_local, g.k_l, st));
-  // line 12: dI = all-reduce_x(dI^), overlapped with line 13 (OAR)
   const int Pb = S.g[h->ax_bwd];
   cudaStream_t bs = S.cstream[h->ax_bwd];
+  const bool rs = S.g[AX_Z] > 1;
+  void* dst = rs ? h->dwpart : dW_hat;
+  const size_t S_el = static_cast<size_t>(g.what_len);
+  cudaEvent_t last = nullptr;
+  // line 11: dI^ = dO x W^T  (M = m_l, N = k_l, K = n_l)
+  auto dI_gemm = [&]() -> axonn_status_t {
+    return run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l, dI_local,
+                    g.k_l, st);
+  };
+  // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
+  auto dW_gemm = [&]() -> axonn_status_t {
+    return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
+                    st);
+  };
+  // line 14 (ORS, waited in grads_sync) and the per-layer data-parallel sum
+  auto grad_comm = [&]() -> axonn_status_t {
+    if (rs) {
+      CUDA_TRY(cudaEventRecord(h->ev_rs, st));
+      CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
+      NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_Z],
+                                 S.cstream[AX_Z]));
+      count_comm(1, S.g[AX_Z], S_el, dt);
+      CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_Z]));
+      last = h->ev_grad;
+    }
+    if (S.g[AX_D] > 1) {
+      CUDA_TRY(cudaEventRecord(h->ev_rs, rs ? S.cstream[AX_Z] : st));
+      CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_D], h->ev_rs, 0));
+      NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_D],
+                             S.cstream[AX_D]));
+      count_comm(4, S.g[AX_D], S_el, dt);
+      CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_D]));
+      last = h->ev_grad;
+    }
+    return AXONN_OK;
+  };
   if (Pb > 1) {
+    // line 11, then line 12 on the bwd-axis stream overlapped with line 13 (OAR)
+    STATUS_TRY(dI_gemm());
     CUDA_TRY(cudaEventRecord(h->ev_dw, st));
     CUDA_TRY(cudaStreamWaitEvent(bs, h->ev_dw, 0));
     NCCL_TRY(ncclAllReduce(dI_local, dI_local, static_cast<size_t>(g.m_l * g.k_l), nt, ncclSum,
                            S.axis_comm[h->ax_bwd], bs));
     count_comm(3, Pb, static_cast<size_t>(g.m_l * g.k_l), dt);
     CUDA_TRY(cudaEventRecord(h->ev_ar, bs));
-  }
-  // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
-  const bool rs = S.g[AX_Z] > 1;
-  void* dst = rs ? h->dwpart : dW_hat;
-  STATUS_TRY(run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst,
-                      g.n_l, st));
-  // line 14: dW_hat = reduce-scatter_z(dW partial)   (ORS: waited in grads_sync)
-  const size_t S_el = static_cast<size_t>(g.what_len);
-  cudaEvent_t last = nullptr;
-  if (rs) {
-    CUDA_TRY(cudaEventRecord(h->ev_rs, st));
-    CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
-    NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_Z],
-                               S.cstream[AX_Z]));
-    count_comm(1, S.g[AX_Z], S_el, dt);
-    CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_Z]));
-    last = h->ev_grad;
-  }
-  // data parallelism: sum dW_hat over the replicas, per layer
-  if (S.g[AX_D] > 1) {
-    CUDA_TRY(cudaEventRecord(h->ev_rs, rs ? S.cstream[AX_Z] : st));
-    CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_D], h->ev_rs, 0));
-    NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_D],
-                           S.cstream[AX_D]));
-    count_comm(4, S.g[AX_D], S_el, dt);
-    CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_D]));
-    last = h->ev_grad;
+    STATUS_TRY(dW_gemm());
+    STATUS_TRY(grad_comm());
+  } else {
+    // no dI all-reduce to hide: compute dW first so its reduce-scatter /
+    // data-parallel all-reduce overlaps the dI GEMM (same results)
+    STATUS_TRY(dW_gemm());
+    STATUS_TRY(grad_comm());
+    STATUS_TRY(dI_gemm());
   }
   if (last) {
     bool seen = false;
