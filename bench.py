@@ -59,6 +59,16 @@ def emit(obj) -> None:
     f.flush()
 
 
+def copy_raw(dst: int, src: int, nbytes: int, stream) -> None:
+    """cudaMemcpyAsync between raw addresses (a library-owned buffer) on `stream`."""
+    import ctypes
+    rt = ctypes.CDLL("libcudart.so.12")
+    rc = rt.cudaMemcpyAsync(ctypes.c_void_p(dst), ctypes.c_void_p(src), ctypes.c_size_t(nbytes),
+                            4, ctypes.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"cudaMemcpyAsync failed ({rc})")
+
+
 def reduce_max(x: float, device: str = "cuda") -> float:
     """Max of a per-rank float over all ranks (device timing is max over ranks)."""
     import torch
@@ -276,10 +286,17 @@ def main():
     for (mm, k, n, t) in layers:
         hd = ax.axonn_fc_create(mm, k, n, t, ax.AXONN_BF16, args.chunks)
         g = ax.axonn_fc_geometry(hd)
-        L.append({"h": hd, "g": g, "I": rnd(g.m_l, g.k_l), "W": rnd(g.what_len),
-                  "O": torch.empty(g.m_l, g.n_l, dtype=bf, device="cuda"),
-                  "dO": rnd(g.m_l, g.n_l), "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
-                  "dW": torch.empty(g.what_len, dtype=bf, device="cuda")})
+        rec = {"h": hd, "g": g, "I": rnd(g.m_l, g.k_l), "W": rnd(g.what_len),
+               "O": torch.empty(g.m_l, g.n_l, dtype=bf, device="cuda"),
+               "dO": rnd(g.m_l, g.n_l), "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
+               "dW": torch.empty(g.what_len, dtype=bf, device="cuda")}
+        # outputs of fused (NVLS) all-reduces live in handle-owned symmetric
+        # buffers; writing there avoids the final copy (include/axonn.h)
+        for key, which in (("O", 0), ("dI", 1), ("dW", 2)):
+            ptr = ax.axonn_fc_output_buffer(hd, which)
+            if ptr:
+                rec[key] = ptr
+        L.append(rec)
 
     def step(s):
         for i, l in enumerate(L):
@@ -340,7 +357,7 @@ def main():
     if not args.no_e2e:
         hI = [l["I"].cpu().pin_memory() for l in L]
         hdO = [l["dO"].cpu().pin_memory() for l in L]
-        hdW = [torch.empty(l["dW"].shape, dtype=bf).pin_memory() for l in L]
+        hdW = [torch.empty(l["g"].what_len, dtype=bf).pin_memory() for l in L]
         copy = torch.cuda.Stream()
         evI = [torch.cuda.Event() for _ in L]
         evO = [torch.cuda.Event() for _ in L]
@@ -368,7 +385,10 @@ def main():
                     ax.axonn_fc_backward(L[i]["h"], L[i]["dO"], L[i]["dI"], L[i]["dW"], stream)
                 ax.axonn_grads_sync(stream)
                 for i, l in enumerate(L):
-                    hdW[i].copy_(l["dW"], non_blocking=True)
+                    if isinstance(l["dW"], int):
+                        copy_raw(hdW[i].data_ptr(), l["dW"], hdW[i].numel() * 2, stream)
+                    else:
+                        hdW[i].copy_(l["dW"], non_blocking=True)
 
         e2e_step()
         barrier()

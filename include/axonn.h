@@ -134,6 +134,18 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out);
 /* Geometry of this rank for handle `h` (host out). */
 axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
 
+/* Handle-owned output buffers of the fused GEMM + all-reduce path (B200
+ * NVLS): which = 0 -> O_local, 1 -> dI_local, 2 -> dW_hat.  *ptr is NULL when
+ * that output takes the NCCL path (axis size != 2, fp32 mode, a row length
+ * not a multiple of 8, or AXONN_FUSED=0).  Passing the returned pointer as the
+ * output argument of axonn_fc_forward / axonn_fc_backward avoids the final
+ * device-to-device copy; its contents are valid until the next call that
+ * writes that output.  Errors: ARG. */
+axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr);
+/* "fused" if collectives along `axis` (0=X,1=Y,2=Z,3=DATA) of the current grid
+ * are fused into the GEMM epilogue over NVLS, else the reason (host buf). */
+axonn_status_t axonn_fused_status(int axis, char* buf, int cap);
+
 /* OAG: start the Z all-gather of W_hat for the NEXT
  * forward now, on the communication stream, after the work already enqueued
  * on `stream`.  Optional; axonn_fc_forward issues it itself if not prefetched. */

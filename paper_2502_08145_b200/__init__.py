@@ -84,6 +84,8 @@ _PROTOS = {
     "axonn_fc_create": (_S, [POINTER(FcDesc), POINTER(c_void_p)]),
     "axonn_fc_geometry": (_S, [c_void_p, POINTER(GeometryT)]),
     "axonn_fc_prefetch": (_S, [c_void_p, c_void_p, c_void_p]),
+    "axonn_fc_output_buffer": (_S, [c_void_p, c_int, POINTER(c_void_p)]),
+    "axonn_fused_status": (_S, [c_int, c_char_p, c_int]),
     "axonn_fc_forward": (_S, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "axonn_fc_backward": (_S, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "axonn_grads_sync": (_S, [c_void_p]),
@@ -199,6 +201,20 @@ def axonn_fc_geometry(h) -> Geometry:
     g = GeometryT()
     _check(_lib.axonn_fc_geometry(c_void_p(h), byref(g)))
     return Geometry(*[getattr(g, f) for f in Geometry._fields])
+
+
+def axonn_fc_output_buffer(h, which: int):
+    """Device address of the handle-owned fused output buffer (0=O, 1=dI, 2=dŴ) or None."""
+    p = c_void_p()
+    _check(_lib.axonn_fc_output_buffer(c_void_p(h), which, byref(p)))
+    return p.value
+
+
+def axonn_fused_status(axis) -> str:
+    a = AXIS[axis] if isinstance(axis, str) else int(axis)
+    buf = ctypes.create_string_buffer(256)
+    _check(_lib.axonn_fused_status(a, buf, 256))
+    return buf.value.decode()
 
 
 def axonn_fc_prefetch(h, W_hat, stream=None) -> None:

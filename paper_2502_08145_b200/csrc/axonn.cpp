@@ -26,8 +26,10 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <algorithm>
 #include <set>
 #include <string>
 #include <vector>
@@ -35,6 +37,7 @@
 #include "../../include/axonn.h"
 #include "gemm.h"
 #include "perf_model.h"
+#include "sym.h"
 
 namespace {
 
@@ -86,6 +89,8 @@ struct State {
   int c[4] = {0, 0, 0, 0};
   ncclComm_t axis_comm[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
+  axonn::SymAxis sym[4];          // NVLS symmetric memory per axis (fused all-reduce)
+  std::string sym_why[4];         // why an axis has no fused path
   std::vector<cudaEvent_t> pending_grads;
   std::set<struct ::axonn_fc*> handles;
   bool profiling = false;
@@ -97,6 +102,11 @@ struct State {
 State S;
 std::recursive_mutex g_mu;
 std::atomic<int64_t> g_launches{0};
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline size_t elem_size(int dtype) { return dtype == AXONN_F32 ? 4 : 2; }
@@ -150,12 +160,13 @@ axonn_status_t check_async_nccl() {
 // One local product on `st`, instrumented.  K == 0 writes zeros.
 axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                         int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                        cudaStream_t st) {
+                        cudaStream_t st, void* red_mc = nullptr) {
   STATUS_TRY(ensure_device());
   if (M == 0 || N == 0) return AXONN_OK;
   const size_t es = elem_size(dtype);
   if (K == 0) {
-    CUDA_TRY(cudaMemset2DAsync(C, ldc * es, 0, N * es, M, st));
+    // a zero partial: nothing to add into a fused (pre-zeroed) reduction buffer
+    if (!red_mc) CUDA_TRY(cudaMemset2DAsync(C, ldc * es, 0, N * es, M, st));
     return AXONN_OK;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -172,7 +183,7 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
   }
   axonn::GemmStatus gs;
   if (dtype == AXONN_BF16)
-    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st);
+    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st, red_mc);
   else
     gs = axonn::gemm_f32_simt(op, M, N, K, static_cast<const float*>(A), lda,
                               static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc, st);
@@ -268,9 +279,19 @@ struct axonn_fc {
   cudaEvent_t ev_in = nullptr, ev_ag = nullptr, ev_ar = nullptr, ev_dw = nullptr,
               ev_rs = nullptr, ev_grad = nullptr;
   std::vector<cudaEvent_t> ev_chunk;
+  // fused all-reduce targets (symmetric, multicast-mapped); ptr == null: NCCL path
+  axonn::SymBuf osym;    // O   over the forward axis
+  axonn::SymBuf disym;   // dI  over the backward axis
+  axonn::SymBuf dwsym;   // dŴ  over DATA (when Gz == 1)
 };
 
 namespace {
+
+axonn_status_t fused_barrier(int axis, cudaStream_t st) {
+  CUDA_TRY(axonn::sym_barrier(&S.sym[axis], st));
+  g_launches.fetch_add(1);
+  return AXONN_OK;
+}
 
 axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) {
   if (S.g[AX_Z] == 1) {
@@ -377,12 +398,33 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
   int lo = 0, hi = 0;
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   for (int a = 0; a < 4; ++a) {
+    S.sym_why[a] = "axis of size 1: no collective";
     if (g[a] > 1) {
       int cc[4] = {S.c[0], S.c[1], S.c[2], S.c[3]};
       cc[a] = 0;
       const int color = coords_to_rank(g, cc);
+      // Axis communicators run beside the persistent GEMM: their CTA budget is
+      // capped (AXONN_NCCL_MAX_CTAS, default 8) so they fit in the SMs the GEMM
+      // leaves free (axonn_set_gemm_sms).
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      const int max_ctas = env_int("AXONN_NCCL_MAX_CTAS", 8);
+      if (max_ctas > 0) {
+        cfg.maxCTAs = max_ctas;
+        cfg.minCTAs = std::min(max_ctas, env_int("AXONN_NCCL_MIN_CTAS", 1));
+        cfg.nvlsCTAs = max_ctas;
+      }
       NCCL_TRY(ncclCommSplit(S.world_comm, color, S.c[a], &S.axis_comm[a], &cfg));
+      // Fused GEMM + all-reduce over NVLS for 2-rank axes (AXONN_FUSED=0 disables).
+      // With two ranks the switch computes RNE(a + b): bit-identical to NCCL.
+      S.sym_why[a].clear();
+      if (g[a] != 2)
+        S.sym_why[a] = "fused all-reduce implemented for 2-rank axes";
+      else if (a == AX_Z || (a == AX_D && g[AX_Z] > 1))
+        S.sym_why[a] = "reduce-scatter / all-gather on this axis use NCCL";
+      else if (env_int("AXONN_FUSED", 1) == 0)
+        S.sym_why[a] = "disabled by AXONN_FUSED=0";
+      else
+        axonn::sym_axis_init(S.axis_comm[a], &S.sym[a], &S.sym_why[a]);
     }
     CUDA_TRY(cudaStreamCreateWithPriority(&S.cstream[a], cudaStreamNonBlocking, hi));
   }
@@ -409,6 +451,7 @@ axonn_status_t axonn_grid_finalize(void) {
   for (auto* h : hs) axonn_fc_destroy(h);
   for (int a = 0; a < 4; ++a) {
     if (S.cstream[a]) cudaStreamSynchronize(S.cstream[a]);
+    axonn::sym_axis_destroy(&S.sym[a]);
     if (S.axis_comm[a]) ncclCommDestroy(S.axis_comm[a]);
     if (S.cstream[a]) cudaStreamDestroy(S.cstream[a]);
     S.axis_comm[a] = nullptr;
@@ -451,6 +494,22 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
   for (cudaEvent_t* e : {&h->ev_in, &h->ev_ag, &h->ev_ar, &h->ev_dw, &h->ev_rs, &h->ev_grad})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
+  if (desc->dtype == AXONN_BF16) {
+    std::string why;
+    const size_t es = elem_size(desc->dtype);
+    auto want = [&](int axis, int64_t cols) {
+      return S.sym[axis].impl != nullptr && cols % 8 == 0;
+    };
+    if (want(h->ax_fwd, geo.n_l) && geo.m_l * geo.n_l > 0 &&
+        !axonn::sym_alloc(&S.sym[h->ax_fwd], geo.m_l * geo.n_l * es, &h->osym, &why))
+      return cleanup(fail(AXONN_ERR_NCCL, "symmetric O buffer: %s", why.c_str()));
+    if (want(h->ax_bwd, geo.k_l) && geo.m_l * geo.k_l > 0 &&
+        !axonn::sym_alloc(&S.sym[h->ax_bwd], geo.m_l * geo.k_l * es, &h->disym, &why))
+      return cleanup(fail(AXONN_ERR_NCCL, "symmetric dI buffer: %s", why.c_str()));
+    if (S.g[AX_Z] == 1 && want(AX_D, geo.n_l) && geo.k_l * geo.n_l > 0 &&
+        !axonn::sym_alloc(&S.sym[AX_D], geo.k_l * geo.n_l * es, &h->dwsym, &why))
+      return cleanup(fail(AXONN_ERR_NCCL, "symmetric dW buffer: %s", why.c_str()));
+  }
   h->ev_chunk.resize(h->d.chunks + 1, nullptr);
   for (auto& e : h->ev_chunk)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
@@ -462,6 +521,20 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
 axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out) {
   if (!h || !out) return fail(AXONN_ERR_ARG, "NULL argument");
   *out = h->geo;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr) {
+  if (!h || !ptr || which < 0 || which > 2) return fail(AXONN_ERR_ARG, "bad argument");
+  const axonn::SymBuf* b = which == 0 ? &h->osym : which == 1 ? &h->disym : &h->dwsym;
+  *ptr = b->ptr;
+  return AXONN_OK;
+}
+
+axonn_status_t axonn_fused_status(int axis, char* buf, int cap) {
+  if (axis < 0 || axis > 3 || !buf || cap < 1) return fail(AXONN_ERR_ARG, "bad argument");
+  const std::string m = S.sym[axis].impl ? std::string("fused") : S.sym_why[axis];
+  std::snprintf(buf, static_cast<size_t>(cap), "%s", m.c_str());
   return AXONN_OK;
 }
 
@@ -487,9 +560,28 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
   h->prefetched = false;
   const void* W = S.g[AX_Z] > 1 ? h->wbuf : W_hat;
   if (S.g[AX_Z] > 1) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ag, 0));
-  // line 3 + line 4, pipelined over M-chunks when requested
   const int P = S.g[h->ax_fwd];
   const size_t es = elem_size(h->d.dtype);
+  if (h->osym.ptr) {
+    // line 3 + line 4 fused: the GEMM epilogue adds each bf16 tile of Ô into
+    // every rank's symmetric copy through NVSwitch (multimem.red); the
+    // barriers order zeroing before any rank's reductions and all reductions
+    // before the result is read.
+    const size_t bytes = static_cast<size_t>(g.m_l * g.n_l) * es;
+    CUDA_TRY(cudaMemsetAsync(h->osym.ptr, 0, bytes, st));
+    STATUS_TRY(fused_barrier(h->ax_fwd, st));
+    STATUS_TRY(run_gemm(AXONN_OP_NN, h->d.dtype, g.m_l, g.n_l, g.k_l, I_local, g.k_l, W, g.n_l,
+                        h->osym.ptr, g.n_l, st, h->osym.mc));
+    STATUS_TRY(fused_barrier(h->ax_fwd, st));
+    count_comm(2, P, static_cast<size_t>(g.m_l * g.n_l), h->d.dtype);
+    if (O_local != h->osym.ptr)
+      CUDA_TRY(cudaMemcpyAsync(O_local, h->osym.ptr, bytes, cudaMemcpyDeviceToDevice, st));
+    h->I = I_local;
+    h->W = W;
+    h->have_fwd = true;
+    return AXONN_OK;
+  }
+  // line 3 + line 4 over NCCL, pipelined over M-chunks when requested
   int chunks = (P > 1) ? h->d.chunks : 1;
   int64_t rows_per = (g.m_l + chunks - 1) / chunks;
   rows_per = (rows_per + 127) / 128 * 128;  // whole 128-row GEMM tiles per chunk
@@ -539,18 +631,21 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   const int Pb = S.g[h->ax_bwd];
   cudaStream_t bs = S.cstream[h->ax_bwd];
   const bool rs = S.g[AX_Z] > 1;
-  void* dst = rs ? h->dwpart : dW_hat;
+  const bool fI = h->disym.ptr != nullptr;   // dI all-reduce fused into the dI GEMM
+  const bool fW = h->dwsym.ptr != nullptr;   // data-parallel dŴ all-reduce fused into the dW GEMM
+  const size_t es = elem_size(dt);
+  void* dst = fW ? h->dwsym.ptr : (rs ? h->dwpart : dW_hat);
   const size_t S_el = static_cast<size_t>(g.what_len);
   cudaEvent_t last = nullptr;
   // line 11: dI^ = dO x W^T  (M = m_l, N = k_l, K = n_l)
   auto dI_gemm = [&]() -> axonn_status_t {
-    return run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l, dI_local,
-                    g.k_l, st);
+    return run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
+                    fI ? h->disym.ptr : dI_local, g.k_l, st, fI ? h->disym.mc : nullptr);
   };
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
   auto dW_gemm = [&]() -> axonn_status_t {
     return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
-                    st);
+                    st, fW ? h->dwsym.mc : nullptr);
   };
   // line 14 (ORS, waited in grads_sync) and the per-layer data-parallel sum
   auto grad_comm = [&]() -> axonn_status_t {
@@ -574,7 +669,12 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     }
     return AXONN_OK;
   };
-  if (Pb > 1) {
+  // fused outputs: zero every rank's copy, then a barrier, before any reduction
+  if (fI) CUDA_TRY(cudaMemsetAsync(h->disym.ptr, 0, static_cast<size_t>(g.m_l * g.k_l) * es, st));
+  if (fW) CUDA_TRY(cudaMemsetAsync(h->dwsym.ptr, 0, S_el * es, st));
+  if (fI) STATUS_TRY(fused_barrier(h->ax_bwd, st));
+  if (fW) STATUS_TRY(fused_barrier(AX_D, st));
+  if (Pb > 1 && !fI) {
     // line 11, then line 12 on the bwd-axis stream overlapped with line 13 (OAR)
     STATUS_TRY(dI_gemm());
     CUDA_TRY(cudaEventRecord(h->ev_dw, st));
@@ -584,21 +684,36 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     count_comm(3, Pb, static_cast<size_t>(g.m_l * g.k_l), dt);
     CUDA_TRY(cudaEventRecord(h->ev_ar, bs));
     STATUS_TRY(dW_gemm());
-    STATUS_TRY(grad_comm());
+    if (!fW) STATUS_TRY(grad_comm());
+  } else if (Pb > 1) {
+    // line 12 fused into line 11; line 13 follows, its reduction overlaps nothing to wait on
+    STATUS_TRY(dI_gemm());
+    count_comm(3, Pb, static_cast<size_t>(g.m_l * g.k_l), dt);
+    STATUS_TRY(dW_gemm());
+    if (!fW) STATUS_TRY(grad_comm());
   } else {
     // no dI all-reduce to hide: compute dW first so its reduce-scatter /
     // data-parallel all-reduce overlaps the dI GEMM (same results)
     STATUS_TRY(dW_gemm());
-    STATUS_TRY(grad_comm());
+    if (!fW) STATUS_TRY(grad_comm());
     STATUS_TRY(dI_gemm());
   }
+  if (fW) count_comm(4, S.g[AX_D], S_el, dt);
+  // fused outputs: every rank's reductions have landed after these barriers
+  if (fI) STATUS_TRY(fused_barrier(h->ax_bwd, st));
+  if (fW) STATUS_TRY(fused_barrier(AX_D, st));
+  if (fI && dI_local != h->disym.ptr)
+    CUDA_TRY(cudaMemcpyAsync(dI_local, h->disym.ptr, static_cast<size_t>(g.m_l * g.k_l) * es,
+                             cudaMemcpyDeviceToDevice, st));
+  if (fW && dW_hat != h->dwsym.ptr)
+    CUDA_TRY(cudaMemcpyAsync(dW_hat, h->dwsym.ptr, S_el * es, cudaMemcpyDeviceToDevice, st));
   if (last) {
     bool seen = false;
     for (auto e : S.pending_grads) seen = seen || (e == last);
     if (!seen) S.pending_grads.push_back(last);
   }
   // dI must be complete in `stream` order when we return
-  if (Pb > 1) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ar, 0));
+  if (Pb > 1 && !fI) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ar, 0));
   h->have_fwd = false;
   return AXONN_OK;
 }
@@ -627,6 +742,9 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
     if (e) cudaEventDestroy(e);
   if (h->wbuf) cudaFree(h->wbuf);
   if (h->dwpart) cudaFree(h->dwpart);
+  axonn::sym_free(&S.sym[h->ax_fwd], &h->osym);
+  axonn::sym_free(&S.sym[h->ax_bwd], &h->disym);
+  axonn::sym_free(&S.sym[AX_D], &h->dwsym);
   delete h;
   return AXONN_OK;
 }

@@ -261,7 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
-                           int group_m) {
+                           int group_m, uint64_t red_mc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -394,7 +394,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         ptx::tmem_wait_ld();
         const int col0 = tc.n0 + c * 32;
         if (row < M && col0 < N) {
-          if (vec_ok && col0 + 32 <= N) {
+          if (red_mc) {
+            // fused all-reduce: NVSwitch adds this partial into every rank's
+            // copy (host guarantees N % 8 == 0 and 16-B aligned rows)
+            const uint64_t base = red_mc + (static_cast<uint64_t>(row) * ldc + col0) * 2;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (col0 + 8 * q < N) {
+                uint4 w;
+                w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                ptx::multimem_red_add_bf16x8(base + 16 * q, w);
+              }
+            }
+          } else if (vec_ok && col0 + 32 <= N) {
             uint4* dst = reinterpret_cast<uint4*>(crow + col0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -418,6 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (red_mc) ptx::fence_sys();  // every reduction performed before the kernel retires
   }
 
   ptx::tc_fence_before();
@@ -477,7 +493,8 @@ cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C,
 
 template <int A_MN, int B_MN>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
-                        int M, int N, int K, int num_sms, int group_m, cudaStream_t stream) {
+                        int M, int N, int K, int num_sms, int group_m, void* red_mc,
+                        cudaStream_t stream) {
   auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -491,7 +508,8 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, i
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
   kern<<<grid, THREADS, P_SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
-                                                N, K, group_m);
+                                                N, K, group_m,
+                                                reinterpret_cast<uint64_t>(red_mc));
   return cudaGetLastError();
 }
 
@@ -507,7 +525,7 @@ int env_int(const char* name, int dflt) {
 // the default is the CTA-pair kernel.  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, void* red_mc) {
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return GemmStatus::kBadShape;
   if ((lda & 7) || (ldb & 7) || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
@@ -537,14 +555,15 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   }
   if (!ok) return GemmStatus::kTensorMap;
   cudaError_t e;
+  if (red_mc && (single || (N & 7) || (ldc & 7))) return GemmStatus::kBadAlignment;
   if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
                   : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
   } else {
-    e = op == 0 ? launch_pair<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, stream)
-        : op == 1 ? launch_pair<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, group_m, stream)
-                  : launch_pair<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, stream);
+    e = op == 0 ? launch_pair<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, red_mc, stream)
+        : op == 1 ? launch_pair<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, group_m, red_mc, stream)
+                  : launch_pair<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, red_mc, stream);
   }
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
 }

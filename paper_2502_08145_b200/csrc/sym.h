@@ -1,0 +1,33 @@
+// sym.h — symmetric NVLink memory for the fused GEMM + all-reduce (see sym.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstddef>
+#include <string>
+
+namespace axonn {
+
+struct SymAxisImpl;
+
+struct SymAxis {
+  SymAxisImpl* impl = nullptr;  // null: no fused path on this axis
+  int nranks = 0;
+};
+
+struct SymBuf {
+  void* ptr = nullptr;  // this rank's copy (device pointer)
+  void* mc = nullptr;   // multicast address: a multimem.red lands in every rank's copy
+  size_t bytes = 0;
+  void* win = nullptr;  // ncclWindow_t
+};
+
+bool sym_axis_init(ncclComm_t comm, SymAxis* out, std::string* why);
+void sym_axis_destroy(SymAxis* a);
+bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why);
+void sym_free(SymAxis* a, SymBuf* b);
+// One-CTA cross-rank barrier on `st` (system-scope release/acquire).
+cudaError_t sym_barrier(SymAxis* a, cudaStream_t st);
+
+}  // namespace axonn

@@ -38,7 +38,7 @@ def host(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world):
+def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_copy=False):
     X, W, dY = synthdata.layer_tensors(m, k, n, 7, kind=kind)
     dt = ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16
     h = ax.axonn_fc_create(m, k, n, transposed, dt, chunks)
@@ -51,16 +51,31 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world):
     O = torch.full((g.m_l, g.n_l), float("nan"), dtype=dtype, device="cuda")
     dI = torch.full((g.m_l, g.k_l), float("nan"), dtype=dtype, device="cuda")
     dW = torch.full((g.what_len,), float("nan"), dtype=dtype, device="cuda")
+    fused = [ax.axonn_fc_output_buffer(h, w) for w in range(3)]
+    outs = [O, dI, dW]
+    if zero_copy:   # write straight into the handle-owned symmetric buffers
+        for w in range(3):
+            if fused[w]:
+                outs[w] = fused[w]
     ax.axonn_comm_bytes(reset=True)
     s = torch.cuda.current_stream()
     ax.axonn_fc_prefetch(h, What, s)           # OAG path
-    ax.axonn_fc_forward(h, I, What, O, s)
-    ax.axonn_fc_backward(h, dO, dI, dW, s)
+    ax.axonn_fc_forward(h, I, What, outs[0], s)
+    ax.axonn_fc_backward(h, dO, outs[1], outs[2], s)
     ax.axonn_grads_sync(s)
     torch.cuda.synchronize()
     sent = ax.axonn_comm_bytes(reset=True)
+    for w, shape in ((0, O.shape), (1, dI.shape), (2, dW.shape)):
+        if zero_copy and fused[w]:   # read the symmetric buffer back into the tensor
+            n_el = int(np.prod(shape))
+            src = torch.empty(n_el, dtype=dtype, device="cuda")
+            import ctypes
+            ctypes.CDLL("libcudart.so.12").cudaMemcpy(ctypes.c_void_p(src.data_ptr()),
+                                                      ctypes.c_void_p(fused[w]),
+                                                      ctypes.c_size_t(n_el * src.element_size()), 3)
+            (O, dI, dW)[w].copy_(src.view(shape))
     ax.axonn_fc_destroy(h)
-    mine = (tuple(g), host(O), host(dI), host(dW), sent)
+    mine = (tuple(g), host(O), host(dI), host(dW), sent, [f is not None for f in fused])
     allv = [None] * world
     dist.all_gather_object(allv, mine)
     if rank != 0:
@@ -72,7 +87,7 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world):
     L = pm.Layer(m, k, n, transposed)
     eq = pm.layer_bytes(L, cfg, b=2 if dt == ax.AXONN_BF16 else 4)
     tag = f"cfg={cfg} shape={(m, k, n)} T={transposed} {kind}/{dtype} chunks={chunks}"
-    for r, (gg, o, di, dw, snt) in enumerate(allv):
+    for r, (gg, o, di, dw, snt, _) in enumerate(allv):
         gg = ax.Geometry(*gg)
         for dst, val, r0, c0 in ((Og, o, gg.row0, gg.out_col0), (dIg, di, gg.row0, gg.in_col0)):
             blk = dst[r0:r0 + val.shape[0], c0:c0 + val.shape[1]]
@@ -98,7 +113,9 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world):
         else:
             err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
             assert err <= 2e-2, f"{name} normwise {err}: {tag}"
-    print(f"ok {tag}", flush=True)
+    nf = sum(allv[0][5])
+    print(f"ok {tag} fused_outputs={nf}", flush=True)
+    return Og, dIg, dWg
 
 
 def main():
@@ -110,16 +127,39 @@ def main():
     ax.bootstrap_from_torch_distributed(local)
     shapes = [(256, 512, 1024), (384, 192, 320)]
     for cfg in ogrid.enumerate_configs(world):
-        ax.axonn_grid_init(*cfg)
-        for (m, k, n) in shapes:
-            for transposed in (False, True):
-                if not pm.feasible(pm.Layer(m, k, n, transposed), cfg):
+        results = {}
+        for fused in ("1", "0"):
+            os.environ["AXONN_FUSED"] = fused
+            ax.axonn_grid_init(*cfg)
+            if fused == "1" and rank == 0:
+                print(f"cfg={cfg} fused status:",
+                      {a: ax.axonn_fused_status(a) for a in "xyzd"}, flush=True)
+            for (m, k, n) in shapes:
+                for transposed in (False, True):
+                    if not pm.feasible(pm.Layer(m, k, n, transposed), cfg):
+                        continue
+                    if fused == "0":
+                        run_case(cfg, m, k, n, transposed, "int", torch.float32, 1, rank, world)
+                    results[(fused, m, k, n, transposed)] = run_case(
+                        cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank, world)
+                    if fused == "1":
+                        zc = run_case(cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank,
+                                      world, zero_copy=True)
+                        if rank == 0:
+                            for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
+                                assert np.array_equal(a, b), f"zero-copy differs {cfg}"
+            if fused == "0":
+                run_case(cfg, 512, 256, 512, False, "int", torch.float32, 3, rank, world)
+                run_case(cfg, 512, 256, 512, False, "uniform", torch.bfloat16, 3, rank, world)
+            ax.axonn_grid_finalize()
+        if rank == 0:   # fused (NVLS) and NCCL paths: bit-identical for 2-rank axes
+            for key, val in results.items():
+                if key[0] != "1":
                     continue
-                run_case(cfg, m, k, n, transposed, "int", torch.float32, 1, rank, world)
-                run_case(cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank, world)
-        run_case(cfg, 512, 256, 512, False, "int", torch.float32, 3, rank, world)
-        run_case(cfg, 512, 256, 512, False, "uniform", torch.bfloat16, 3, rank, world)
-        ax.axonn_grid_finalize()
+                ref = results[("0",) + key[1:]]
+                for name, a, b in zip(("O", "dI", "dW"), val, ref):
+                    assert np.array_equal(a, b), f"fused != NCCL for {name} at {cfg} {key}"
+            print(f"fused==nccl bit-exact cfg={cfg}", flush=True)
     dist.barrier()
     if rank == 0:
         print("MP_OK", flush=True)
