@@ -146,6 +146,13 @@ axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr);
  * are fused into the GEMM epilogue over NVLS, else the reason (host buf). */
 axonn_status_t axonn_fused_status(int axis, char* buf, int cap);
 
+/* Diagnostics: bytes/s one rank moves over NVLink with one primitive on the
+ * symmetric memory of `axis` (mode 0: multimem.red.add bf16, 1: multimem.st,
+ * 2: plain 16-B stores to the next rank's copy, 3: multimem.ld_reduce,
+ * 4: local stores), `ctas` x 512 threads.  Collective over the axis. */
+axonn_status_t axonn_nvlink_probe(int axis, int64_t bytes, int mode, int ctas, int iters,
+                                  double* gbps);
+
 /* OAG: start the Z all-gather of W_hat for the NEXT
  * forward now, on the communication stream, after the work already enqueued
  * on `stream`.  Optional; axonn_fc_forward issues it itself if not prefetched. */

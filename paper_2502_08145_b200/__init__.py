@@ -86,6 +86,7 @@ _PROTOS = {
     "axonn_fc_prefetch": (_S, [c_void_p, c_void_p, c_void_p]),
     "axonn_fc_output_buffer": (_S, [c_void_p, c_int, POINTER(c_void_p)]),
     "axonn_fused_status": (_S, [c_int, c_char_p, c_int]),
+    "axonn_nvlink_probe": (_S, [c_int, c_int64, c_int, c_int, c_int, POINTER(c_double)]),
     "axonn_fc_forward": (_S, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "axonn_fc_backward": (_S, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "axonn_grads_sync": (_S, [c_void_p]),
@@ -208,6 +209,13 @@ def axonn_fc_output_buffer(h, which: int):
     p = c_void_p()
     _check(_lib.axonn_fc_output_buffer(c_void_p(h), which, byref(p)))
     return p.value
+
+
+def axonn_nvlink_probe(axis, nbytes, mode, ctas=148, iters=10) -> float:
+    a = AXIS[axis] if isinstance(axis, str) else int(axis)
+    v = c_double()
+    _check(_lib.axonn_nvlink_probe(a, nbytes, mode, ctas, iters, byref(v)))
+    return v.value
 
 
 def axonn_fused_status(axis) -> str:

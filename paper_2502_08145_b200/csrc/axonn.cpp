@@ -531,6 +531,27 @@ axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr) {
   return AXONN_OK;
 }
 
+axonn_status_t axonn_nvlink_probe(int axis, int64_t bytes, int mode, int ctas, int iters,
+                                  double* gbps) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (axis < 0 || axis > 3 || bytes <= 0 || mode < 0 || mode > 4 || ctas < 1 || iters < 1 || !gbps)
+    return fail(AXONN_ERR_ARG, "bad argument");
+  if (!S.sym[axis].impl) return fail(AXONN_ERR_STATE, "axis %d has no symmetric memory: %s", axis,
+                                     S.sym_why[axis].c_str());
+  axonn::SymBuf b;
+  std::string why;
+  if (!axonn::sym_alloc(&S.sym[axis], static_cast<size_t>(bytes), &b, &why))
+    return fail(AXONN_ERR_NCCL, "%s", why.c_str());
+  float ms = 0.f;
+  const int peer = (S.c[axis] + 1) % S.g[axis];
+  cudaError_t e = axonn::sym_probe(&S.sym[axis], &b, mode, peer, ctas, iters, &ms);
+  const double moved = static_cast<double>(b.bytes);
+  axonn::sym_free(&S.sym[axis], &b);
+  if (e != cudaSuccess) return fail(AXONN_ERR_CUDA, "probe: %s", cudaGetErrorString(e));
+  *gbps = moved / (ms * 1e-3) / 1e9;
+  return AXONN_OK;
+}
+
 axonn_status_t axonn_fused_status(int axis, char* buf, int cap) {
   if (axis < 0 || axis > 3 || !buf || cap < 1) return fail(AXONN_ERR_ARG, "bad argument");
   const std::string m = S.sym[axis].impl ? std::string("fused") : S.sym_why[axis];

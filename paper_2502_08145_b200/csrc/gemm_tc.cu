@@ -254,7 +254,8 @@ constexpr int P_STAGES = 6;
 constexpr int P_SMEM_A = 128 * BK * 2;    // 16 KiB per CTA
 constexpr int P_SMEM_B = 128 * BK * 2;    // 16 KiB per CTA (half of N)
 constexpr int P_STAGE_BYTES = P_SMEM_A + P_SMEM_B;
-constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + 256;
+constexpr int P_EPI_BYTES = 4 * 32 * 64 * 2;  // per epilogue warp: 32 rows x 64 bf16 staging
+constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + P_EPI_BYTES + 256;
 
 template <int A_MN, int B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -267,7 +268,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + P_STAGES * P_SMEM_A;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_SMEM_B);
+  uint8_t* sEpi = sB + P_STAGES * P_SMEM_B;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + P_EPI_BYTES);
   uint64_t* empty = full + P_STAGES;
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -375,57 +377,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (both CTAs)
+    // TMEM -> registers (thread = row) -> bf16 -> XOR-swizzled smem -> 16-B
+    // vectors with 8 consecutive threads covering one 128-B row segment, so
+    // every global store / NVLS reduction is a full line.
     const int e = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+    uint8_t* stage = sEpi + e * (32 * 64 * 2);
+    const uint32_t stage_u32 = ptx::smem_u32(stage);
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, P_BM, P_BN);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row = tc.m0 + 128 * static_cast<int>(rank) + 32 * e + lane;
-      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * ldc;
+      const int row0 = tc.m0 + 128 * static_cast<int>(rank) + 32 * e;
 #pragma unroll 1
-      for (int c = 0; c < P_BN / 32; ++c) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) +
-                               static_cast<uint32_t>(acc * P_BN + c * 32);
-        ptx::tmem_ld_32x32b_x32(taddr, v);
-        ptx::tmem_wait_ld();
-        const int col0 = tc.n0 + c * 32;
-        if (row < M && col0 < N) {
-          if (red_mc) {
-            // fused all-reduce: NVSwitch adds this partial into every rank's
-            // copy (host guarantees N % 8 == 0 and 16-B aligned rows)
-            const uint64_t base = red_mc + (static_cast<uint64_t>(row) * ldc + col0) * 2;
+      for (int c = 0; c < P_BN / 64; ++c) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (col0 + 8 * q < N) {
-                uint4 w;
-                w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-                w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-                w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-                w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-                ptx::multimem_red_add_bf16x8(base + 16 * q, w);
-              }
-            }
-          } else if (vec_ok && col0 + 32 <= N) {
-            uint4* dst = reinterpret_cast<uint4*>(crow + col0);
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t v[32];
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) +
+                                 static_cast<uint32_t>(acc * P_BN + c * 64 + hh * 32);
+          ptx::tmem_ld_32x32b_x32(taddr, v);
+          ptx::tmem_wait_ld();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w;
-              w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-              w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-              w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-              w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-              dst[q] = w;
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (col0 + q < N) crow[col0 + q] = __float2bfloat16_rn(__uint_as_float(v[q]));
+          for (int q = 0; q < 4; ++q) {
+            const int j = hh * 4 + q;  // 16-B unit of this row segment
+            const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                         "r"(ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1])),
+                         "r"(ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
+                         "r"(ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5])),
+                         "r"(ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
+                         : "memory");
           }
         }
+        __syncwarp();
+        const int u = lane & 7;
+        const int gcol = tc.n0 + c * 64 + u * 8;
+#pragma unroll 2
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + (lane >> 3);
+          uint4 w;
+          const uint32_t a = stage_u32 + r * 128 + ((u ^ (r & 7)) << 4);
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                       : "r"(a)
+                       : "memory");
+          const int grow = row0 + r;
+          if (grow < M && gcol < N) {
+            if (red_mc) {
+              // fused all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
+              ptx::multimem_red_add_bf16x8(
+                  red_mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
+            } else if (vec_ok && gcol + 8 <= N) {
+              *reinterpret_cast<uint4*>(C + static_cast<int64_t>(grow) * ldc + gcol) = w;
+            } else {
+              const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+              __nv_bfloat16* dst = C + static_cast<int64_t>(grow) * ldc + gcol;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                if (gcol + q < N) {
+                  const uint16_t bits = static_cast<uint16_t>(ws[q >> 1] >> (16 * (q & 1)));
+                  dst[q] = __ushort_as_bfloat16(bits);
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
       }
       ptx::tc_fence_before();
       __syncwarp();

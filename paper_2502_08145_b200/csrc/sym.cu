@@ -29,6 +29,35 @@ __global__ void k_mc_ptr(ncclWindow_t w, ncclDevComm dc, void** out) {
   out[1] = ncclGetLocalPointer(w, 0);
 }
 
+__global__ void k_peer_ptr(ncclWindow_t w, int peer, void** out) {
+  out[0] = ncclGetLsaPointer(w, 0, peer);
+}
+
+// NVLink primitive throughput probe: every thread moves 16-B vectors.
+__global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n16; i += stride) {
+    uint4 v = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+    const uint64_t a = target + 16 * i;
+    if (mode == 0) {
+      asm volatile("multimem.red.relaxed.sys.global.add.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(a),
+                   "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    } else if (mode == 1) {
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(a),
+                   "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    } else if (mode == 2) {
+      *reinterpret_cast<uint4*>(a) = v;               // plain store to a peer (LSA) address
+    } else if (mode == 3) {
+      uint32_t x0, x1, x2, x3;
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "l"(a) : "memory");
+      local[i] = make_uint4(x0, x1, x2, x3);
+    } else {
+      local[i] = v;                                    // local HBM store, for reference
+    }
+  }
+}
+
 __global__ void k_barrier(ncclDevComm dc) {
   ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), 0);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
@@ -125,6 +154,39 @@ void sym_free(SymAxis* a, SymBuf* b) {
   if (a->impl) ncclCommWindowDeregister(a->impl->comm, static_cast<ncclWindow_t>(b->win));
   ncclMemFree(b->ptr);
   *b = SymBuf();
+}
+
+void* sym_peer_ptr(SymBuf* b, int peer) {
+  void** d = nullptr;
+  void* h = nullptr;
+  if (cudaMalloc(&d, sizeof(void*)) != cudaSuccess) return nullptr;
+  k_peer_ptr<<<1, 1>>>(static_cast<ncclWindow_t>(b->win), peer, d);
+  cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h;
+}
+
+cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms) {
+  uint64_t target = reinterpret_cast<uint64_t>(b->mc);
+  if (mode == 2) target = reinterpret_cast<uint64_t>(sym_peer_ptr(b, peer));
+  if (mode == 4) target = reinterpret_cast<uint64_t>(b->ptr);
+  const size_t n16 = b->bytes / 16;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  sym_barrier(a, 0);
+  k_probe<<<ctas, 512>>>(static_cast<uint4*>(b->ptr), target, n16, mode);
+  sym_barrier(a, 0);
+  cudaEventRecord(e0, 0);
+  for (int i = 0; i < iters; ++i) k_probe<<<ctas, 512>>>(static_cast<uint4*>(b->ptr), target, n16, mode);
+  cudaEventRecord(e1, 0);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(ms, e0, e1);
+  *ms /= iters;
+  sym_barrier(a, 0);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaDeviceSynchronize();
 }
 
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st) {

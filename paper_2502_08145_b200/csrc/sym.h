@@ -27,6 +27,11 @@ bool sym_axis_init(ncclComm_t comm, SymAxis* out, std::string* why);
 void sym_axis_destroy(SymAxis* a);
 bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why);
 void sym_free(SymAxis* a, SymBuf* b);
+// Diagnostics: device address of `peer`'s copy; NVLink primitive throughput
+// probe over the whole buffer (mode 0 multimem.red bf16, 1 multimem.st,
+// 2 plain store to peer, 3 multimem.ld_reduce, 4 local store).
+void* sym_peer_ptr(SymBuf* b, int peer);
+cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms);
 // One-CTA cross-rank barrier on `st` (system-scope release/acquire).
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st);
 
