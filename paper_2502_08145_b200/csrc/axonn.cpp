@@ -160,13 +160,16 @@ axonn_status_t check_async_nccl() {
 // One local product on `st`, instrumented.  K == 0 writes zeros.
 axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                         int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                        cudaStream_t st, void* red_mc = nullptr) {
+                        cudaStream_t st, const axonn::EpiTarget* epi = nullptr) {
   STATUS_TRY(ensure_device());
   if (M == 0 || N == 0) return AXONN_OK;
   const size_t es = elem_size(dtype);
   if (K == 0) {
     // a zero partial: nothing to add into a fused (pre-zeroed) reduction buffer
-    if (!red_mc) CUDA_TRY(cudaMemset2DAsync(C, ldc * es, 0, N * es, M, st));
+    if (epi && epi->mode == axonn::kScatter)
+      return fail(AXONN_ERR_UNSUPPORTED, "fused reduce-scatter of an empty product");
+    if (!epi || epi->mode == axonn::kStore)
+      CUDA_TRY(cudaMemset2DAsync(C, ldc * es, 0, N * es, M, st));
     return AXONN_OK;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -183,7 +186,7 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
   }
   axonn::GemmStatus gs;
   if (dtype == AXONN_BF16)
-    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st, red_mc);
+    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st, epi);
   else
     gs = axonn::gemm_f32_simt(op, M, N, K, static_cast<const float*>(A), lda,
                               static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc, st);
@@ -279,10 +282,17 @@ struct axonn_fc {
   cudaEvent_t ev_in = nullptr, ev_ag = nullptr, ev_ar = nullptr, ev_dw = nullptr,
               ev_rs = nullptr, ev_grad = nullptr;
   std::vector<cudaEvent_t> ev_chunk;
-  // fused all-reduce targets (symmetric, multicast-mapped); ptr == null: NCCL path
-  axonn::SymBuf osym;    // O   over the forward axis
-  axonn::SymBuf disym;   // dI  over the backward axis
-  axonn::SymBuf dwsym;   // dŴ  over DATA (when Gz == 1)
+  // fused all-reduces (epi.mode == kStore: NCCL path)
+  struct Fused {
+    int axis = 0;
+    size_t elems = 0;
+    axonn::SymBuf out;    // every rank's result (handle-owned output buffer)
+    axonn::SymBuf recv;   // P-rank scatter mode: P slots of elems / P
+    axonn::EpiTarget epi;
+  };
+  Fused fo;   // O   over the forward axis      (Alg. 1 line 4 fused into line 3)
+  Fused fi;   // dI  over the backward axis     (line 12 fused into line 11)
+  Fused fw;   // dŴ  over DATA when Gz == 1     (PAPER.md:313-317 fused into line 13)
 };
 
 namespace {
@@ -290,6 +300,62 @@ namespace {
 axonn_status_t fused_barrier(int axis, cudaStream_t st) {
   CUDA_TRY(axonn::sym_barrier(&S.sym[axis], st));
   g_launches.fetch_add(1);
+  return AXONN_OK;
+}
+
+// Fused all-reduce of a rows x cols bf16 output over `axis` (see sym.cu):
+// 2 ranks: multimem.red straight from the epilogue (RNE(a + b), exact
+// commutative: bit-identical to NCCL); P >= 3: the epilogue scatters 16-B
+// vectors to their owner rank, the owner sums the P slots in rank order and
+// multicasts the result (every element reduced once: replicas bit-identical).
+bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, std::string* why) {
+  f->axis = axis;
+  f->epi = axonn::EpiTarget();
+  const int P = S.g[axis];
+  const int64_t n = rows * cols;
+  if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % 8) return true;  // NCCL path
+  if (P > 2 && n % (8 * P)) return true;
+  f->elems = static_cast<size_t>(n);
+  if (!axonn::sym_alloc(&S.sym[axis], f->elems * 2, &f->out, why)) return false;
+  if (P == 2) {
+    f->epi.mode = axonn::kMcRed;
+    f->epi.mc = reinterpret_cast<unsigned long long>(f->out.mc);
+    return true;
+  }
+  if (!axonn::sym_alloc(&S.sym[axis], f->elems * 2, &f->recv, why)) return false;
+  f->epi.mode = axonn::kScatter;
+  f->epi.P = P;
+  f->epi.me = S.c[axis];
+  f->epi.slice = n / P;
+  for (int q = 0; q < P; ++q) {
+    f->epi.peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv, q));
+    if (!f->epi.peer[q]) {
+      *why = "peer address of the receive window unavailable";
+      return false;
+    }
+  }
+  return true;
+}
+
+axonn_status_t fused_barrier(int axis, cudaStream_t st);
+
+axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
+  if (f.epi.mode == axonn::kMcRed) {
+    // zero every rank's copy, and order that before any rank's reductions
+    CUDA_TRY(cudaMemsetAsync(f.out.ptr, 0, f.elems * 2, st));
+    return fused_barrier(f.axis, st);
+  }
+  return AXONN_OK;  // scatter: the previous use's final barrier already freed the slots
+}
+
+axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st) {
+  STATUS_TRY(fused_barrier(f.axis, st));  // every rank's epilogue writes have landed
+  if (f.epi.mode == axonn::kScatter) {
+    CUDA_TRY(axonn::sym_owner_reduce(&f.recv, &f.out, f.epi.slice, f.epi.P, f.epi.me, S.num_sms,
+                                     st));
+    g_launches.fetch_add(1);
+    STATUS_TRY(fused_barrier(f.axis, st));  // every owner's broadcast has landed
+  }
   return AXONN_OK;
 }
 
@@ -417,8 +483,8 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
       // Fused GEMM + all-reduce over NVLS for 2-rank axes (AXONN_FUSED=0 disables).
       // With two ranks the switch computes RNE(a + b): bit-identical to NCCL.
       S.sym_why[a].clear();
-      if (g[a] != 2)
-        S.sym_why[a] = "fused all-reduce implemented for 2-rank axes";
+      if (g[a] > 8)
+        S.sym_why[a] = "fused all-reduce implemented for up to 8 ranks";
       else if (a == AX_Z || (a == AX_D && g[AX_Z] > 1))
         S.sym_why[a] = "reduce-scatter / all-gather on this axis use NCCL";
       else if (env_int("AXONN_FUSED", 1) == 0)
@@ -496,19 +562,10 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
   if (desc->dtype == AXONN_BF16) {
     std::string why;
-    const size_t es = elem_size(desc->dtype);
-    auto want = [&](int axis, int64_t cols) {
-      return S.sym[axis].impl != nullptr && cols % 8 == 0;
-    };
-    if (want(h->ax_fwd, geo.n_l) && geo.m_l * geo.n_l > 0 &&
-        !axonn::sym_alloc(&S.sym[h->ax_fwd], geo.m_l * geo.n_l * es, &h->osym, &why))
-      return cleanup(fail(AXONN_ERR_NCCL, "symmetric O buffer: %s", why.c_str()));
-    if (want(h->ax_bwd, geo.k_l) && geo.m_l * geo.k_l > 0 &&
-        !axonn::sym_alloc(&S.sym[h->ax_bwd], geo.m_l * geo.k_l * es, &h->disym, &why))
-      return cleanup(fail(AXONN_ERR_NCCL, "symmetric dI buffer: %s", why.c_str()));
-    if (S.g[AX_Z] == 1 && want(AX_D, geo.n_l) && geo.k_l * geo.n_l > 0 &&
-        !axonn::sym_alloc(&S.sym[AX_D], geo.k_l * geo.n_l * es, &h->dwsym, &why))
-      return cleanup(fail(AXONN_ERR_NCCL, "symmetric dW buffer: %s", why.c_str()));
+    if (!fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, &why) ||
+        !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, &why) ||
+        (S.g[AX_Z] == 1 && !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, &why)))
+      return cleanup(fail(AXONN_ERR_NCCL, "fused all-reduce buffers: %s", why.c_str()));
   }
   h->ev_chunk.resize(h->d.chunks + 1, nullptr);
   for (auto& e : h->ev_chunk)
@@ -526,8 +583,8 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out) {
 
 axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr) {
   if (!h || !ptr || which < 0 || which > 2) return fail(AXONN_ERR_ARG, "bad argument");
-  const axonn::SymBuf* b = which == 0 ? &h->osym : which == 1 ? &h->disym : &h->dwsym;
-  *ptr = b->ptr;
+  const axonn_fc::Fused* f = which == 0 ? &h->fo : which == 1 ? &h->fi : &h->fw;
+  *ptr = f->epi.mode != axonn::kStore ? f->out.ptr : nullptr;
   return AXONN_OK;
 }
 
@@ -583,20 +640,17 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
   if (S.g[AX_Z] > 1) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ag, 0));
   const int P = S.g[h->ax_fwd];
   const size_t es = elem_size(h->d.dtype);
-  if (h->osym.ptr) {
-    // line 3 + line 4 fused: the GEMM epilogue adds each bf16 tile of Ô into
-    // every rank's symmetric copy through NVSwitch (multimem.red); the
-    // barriers order zeroing before any rank's reductions and all reductions
-    // before the result is read.
+  if (h->fo.epi.mode != axonn::kStore) {
+    // line 3 + line 4 fused: the GEMM epilogue sends each bf16 tile of Ô
+    // over NVLink (fused_setup); barriers order the buffer reuse.
     const size_t bytes = static_cast<size_t>(g.m_l * g.n_l) * es;
-    CUDA_TRY(cudaMemsetAsync(h->osym.ptr, 0, bytes, st));
-    STATUS_TRY(fused_barrier(h->ax_fwd, st));
+    STATUS_TRY(fused_pre(h->fo, st));
     STATUS_TRY(run_gemm(AXONN_OP_NN, h->d.dtype, g.m_l, g.n_l, g.k_l, I_local, g.k_l, W, g.n_l,
-                        h->osym.ptr, g.n_l, st, h->osym.mc));
-    STATUS_TRY(fused_barrier(h->ax_fwd, st));
+                        h->fo.out.ptr, g.n_l, st, &h->fo.epi));
+    STATUS_TRY(fused_post(h->fo, st));
     count_comm(2, P, static_cast<size_t>(g.m_l * g.n_l), h->d.dtype);
-    if (O_local != h->osym.ptr)
-      CUDA_TRY(cudaMemcpyAsync(O_local, h->osym.ptr, bytes, cudaMemcpyDeviceToDevice, st));
+    if (O_local != h->fo.out.ptr)
+      CUDA_TRY(cudaMemcpyAsync(O_local, h->fo.out.ptr, bytes, cudaMemcpyDeviceToDevice, st));
     h->I = I_local;
     h->W = W;
     h->have_fwd = true;
@@ -652,21 +706,21 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   const int Pb = S.g[h->ax_bwd];
   cudaStream_t bs = S.cstream[h->ax_bwd];
   const bool rs = S.g[AX_Z] > 1;
-  const bool fI = h->disym.ptr != nullptr;   // dI all-reduce fused into the dI GEMM
-  const bool fW = h->dwsym.ptr != nullptr;   // data-parallel dŴ all-reduce fused into the dW GEMM
+  const bool fI = h->fi.epi.mode != axonn::kStore;  // dI all-reduce fused into the dI GEMM
+  const bool fW = h->fw.epi.mode != axonn::kStore;  // data-parallel dŴ all-reduce fused into the dW GEMM
   const size_t es = elem_size(dt);
-  void* dst = fW ? h->dwsym.ptr : (rs ? h->dwpart : dW_hat);
+  void* dst = fW ? h->fw.out.ptr : (rs ? h->dwpart : dW_hat);
   const size_t S_el = static_cast<size_t>(g.what_len);
   cudaEvent_t last = nullptr;
   // line 11: dI^ = dO x W^T  (M = m_l, N = k_l, K = n_l)
   auto dI_gemm = [&]() -> axonn_status_t {
     return run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
-                    fI ? h->disym.ptr : dI_local, g.k_l, st, fI ? h->disym.mc : nullptr);
+                    fI ? h->fi.out.ptr : dI_local, g.k_l, st, fI ? &h->fi.epi : nullptr);
   };
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
   auto dW_gemm = [&]() -> axonn_status_t {
     return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
-                    st, fW ? h->dwsym.mc : nullptr);
+                    st, fW ? &h->fw.epi : nullptr);
   };
   // line 14 (ORS, waited in grads_sync) and the per-layer data-parallel sum
   auto grad_comm = [&]() -> axonn_status_t {
@@ -690,11 +744,9 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     }
     return AXONN_OK;
   };
-  // fused outputs: zero every rank's copy, then a barrier, before any reduction
-  if (fI) CUDA_TRY(cudaMemsetAsync(h->disym.ptr, 0, static_cast<size_t>(g.m_l * g.k_l) * es, st));
-  if (fW) CUDA_TRY(cudaMemsetAsync(h->dwsym.ptr, 0, S_el * es, st));
-  if (fI) STATUS_TRY(fused_barrier(h->ax_bwd, st));
-  if (fW) STATUS_TRY(fused_barrier(AX_D, st));
+  // fused outputs: buffers ready on every rank before any rank's epilogue writes
+  if (fI) STATUS_TRY(fused_pre(h->fi, st));
+  if (fW) STATUS_TRY(fused_pre(h->fw, st));
   if (Pb > 1 && !fI) {
     // line 11, then line 12 on the bwd-axis stream overlapped with line 13 (OAR)
     STATUS_TRY(dI_gemm());
@@ -720,14 +772,14 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     STATUS_TRY(dI_gemm());
   }
   if (fW) count_comm(4, S.g[AX_D], S_el, dt);
-  // fused outputs: every rank's reductions have landed after these barriers
-  if (fI) STATUS_TRY(fused_barrier(h->ax_bwd, st));
-  if (fW) STATUS_TRY(fused_barrier(AX_D, st));
-  if (fI && dI_local != h->disym.ptr)
-    CUDA_TRY(cudaMemcpyAsync(dI_local, h->disym.ptr, static_cast<size_t>(g.m_l * g.k_l) * es,
+  // fused outputs: every rank's reductions have landed after these
+  if (fI) STATUS_TRY(fused_post(h->fi, st));
+  if (fW) STATUS_TRY(fused_post(h->fw, st));
+  if (fI && dI_local != h->fi.out.ptr)
+    CUDA_TRY(cudaMemcpyAsync(dI_local, h->fi.out.ptr, static_cast<size_t>(g.m_l * g.k_l) * es,
                              cudaMemcpyDeviceToDevice, st));
-  if (fW && dW_hat != h->dwsym.ptr)
-    CUDA_TRY(cudaMemcpyAsync(dW_hat, h->dwsym.ptr, S_el * es, cudaMemcpyDeviceToDevice, st));
+  if (fW && dW_hat != h->fw.out.ptr)
+    CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fw.out.ptr, S_el * es, cudaMemcpyDeviceToDevice, st));
   if (last) {
     bool seen = false;
     for (auto e : S.pending_grads) seen = seen || (e == last);
@@ -763,9 +815,10 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
     if (e) cudaEventDestroy(e);
   if (h->wbuf) cudaFree(h->wbuf);
   if (h->dwpart) cudaFree(h->dwpart);
-  axonn::sym_free(&S.sym[h->ax_fwd], &h->osym);
-  axonn::sym_free(&S.sym[h->ax_bwd], &h->disym);
-  axonn::sym_free(&S.sym[AX_D], &h->dwsym);
+  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw}) {
+    axonn::sym_free(&S.sym[f->axis], &f->out);
+    axonn::sym_free(&S.sym[f->axis], &f->recv);
+  }
   delete h;
   return AXONN_OK;
 }

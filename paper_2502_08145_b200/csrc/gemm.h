@@ -7,15 +7,29 @@
 
 namespace axonn {
 
+// Where the epilogue sends each bf16 tile (see gemm_tc.cu):
+//   kStore     C[M][N] local stores;
+//   kMcRed     multimem.red.add into every rank's copy of a multicast buffer
+//              (2-rank fused all-reduce);
+//   kScatter   plain NVLink stores of each 16-B vector into its owner rank's
+//              receive slot: owner o = flat index / slice, destination
+//              peer[o] + (me * slice + flat - o * slice) (fused reduce-scatter;
+//              needs ldc == N and slice % 8 == 0).
+struct EpiTarget {
+  int mode = 0;
+  int P = 0, me = 0;
+  long long slice = 0;
+  unsigned long long mc = 0;
+  unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2 };
+
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 
 // bf16 x bf16 -> bf16 (fp32 accumulate) on tcgen05; op 0 = NN, 1 = NT, 2 = TN.
-// red_mc != nullptr: instead of storing C, add the bf16-rounded tile into
-// every rank's copy of a multicast-mapped buffer (multimem.red; C/ldc give the
-// local layout, N % 8 == 0).
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream, void* red_mc = nullptr);
+                        cudaStream_t stream, const EpiTarget* epi = nullptr);
 
 // fp32 SIMT FMA (test mode, no TF32): same op codes.
 GemmStatus gemm_f32_simt(int op, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

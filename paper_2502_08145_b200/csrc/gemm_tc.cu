@@ -262,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
-                           int group_m, uint64_t red_mc) {
+                           int group_m, const __grid_constant__ EpiTarget epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -426,10 +426,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                        : "memory");
           const int grow = row0 + r;
           if (grow < M && gcol < N) {
-            if (red_mc) {
-              // fused all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
-              ptx::multimem_red_add_bf16x8(
-                  red_mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
+            if (epi.mode == kMcRed) {
+              // fused 2-rank all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
+              ptx::multimem_red_add_bf16x8(epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2,
+                                           w);
+            } else if (epi.mode == kScatter) {
+              // fused reduce-scatter: this 16-B vector goes to its owner's slot
+              const long long f = static_cast<long long>(grow) * N + gcol;
+              const int o = static_cast<int>(f / epi.slice);
+              const long long off = static_cast<long long>(epi.me) * epi.slice + (f - o * epi.slice);
+              *reinterpret_cast<uint4*>(epi.peer[o] + static_cast<uint64_t>(off) * 2) = w;
             } else if (vec_ok && gcol + 8 <= N) {
               *reinterpret_cast<uint4*>(C + static_cast<int64_t>(grow) * ldc + gcol) = w;
             } else {
@@ -453,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (red_mc) ptx::fence_sys();  // every reduction performed before the kernel retires
+    if (epi.mode != kStore) ptx::fence_sys();  // remote writes performed before the kernel retires
   }
 
   ptx::tc_fence_before();
@@ -513,7 +519,7 @@ cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C,
 
 template <int A_MN, int B_MN>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
-                        int M, int N, int K, int num_sms, int group_m, void* red_mc,
+                        int M, int N, int K, int num_sms, int group_m, const EpiTarget& epi,
                         cudaStream_t stream) {
   auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN>;
   static bool attr_set = false;
@@ -528,8 +534,7 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, i
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
   kern<<<grid, THREADS, P_SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
-                                                N, K, group_m,
-                                                reinterpret_cast<uint64_t>(red_mc));
+                                                N, K, group_m, epi);
   return cudaGetLastError();
 }
 
@@ -545,7 +550,7 @@ int env_int(const char* name, int dflt) {
 // the default is the CTA-pair kernel.  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream, void* red_mc) {
+                        cudaStream_t stream, const EpiTarget* epi_in) {
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return GemmStatus::kBadShape;
   if ((lda & 7) || (ldb & 7) || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
@@ -575,15 +580,18 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   }
   if (!ok) return GemmStatus::kTensorMap;
   cudaError_t e;
-  if (red_mc && (single || (N & 7) || (ldc & 7))) return GemmStatus::kBadAlignment;
+  const EpiTarget epi = epi_in ? *epi_in : EpiTarget();
+  if (epi.mode != kStore && (single || (N & 7) || (ldc & 7))) return GemmStatus::kBadAlignment;
+  if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
+    return GemmStatus::kBadAlignment;
   if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
                   : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
   } else {
-    e = op == 0 ? launch_pair<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, red_mc, stream)
-        : op == 1 ? launch_pair<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, group_m, red_mc, stream)
-                  : launch_pair<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, red_mc, stream);
+    e = op == 0 ? launch_pair<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
+        : op == 1 ? launch_pair<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
+                  : launch_pair<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream);
   }
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
 }

@@ -11,6 +11,7 @@
 //   * a one-CTA barrier kernel (release/acquire at system scope) that orders
 //     "buffer zeroed on every rank" before the GEMM and "every rank's
 //     reductions landed" after it.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <nccl_device.h>
@@ -56,6 +57,39 @@ __global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
       local[i] = v;                                    // local HBM store, for reference
     }
   }
+}
+
+// Owner phase of the P-rank fused all-reduce: sum the P slots this rank
+// received (fixed order src = 0..P-1, fp32, one RNE rounding to bf16) and
+// broadcast the result into every rank's output copy with multimem.st.  Every
+// element is reduced by exactly one rank, so all replicas hold the same bits.
+__global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, int P,
+                               unsigned long long out_mc) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n16;
+       i += stride) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int src = 0; src < P; ++src) {
+      const uint4 v = recv[src * n16 + i];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[2 * q] += __uint_as_float(w[q] << 16);
+        acc[2 * q + 1] += __uint_as_float(w[q] & 0xFFFF0000u);
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+      o[q] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
+                     out_mc + static_cast<unsigned long long>(i) * 16),
+                 "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                 : "memory");
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
 __global__ void k_barrier(ncclDevComm dc) {
@@ -187,6 +221,19 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return cudaDeviceSynchronize();
+}
+
+cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
+                             int me, int num_sms, cudaStream_t st) {
+  const long long n16 = slice / 8;
+  long long blocks = (n16 + 255) / 256;
+  if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
+  if (blocks < 1) blocks = 1;
+  const unsigned long long mc =
+      reinterpret_cast<unsigned long long>(out->mc) + static_cast<unsigned long long>(me) * slice * 2;
+  k_owner_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(recv->ptr) , n16, P, mc);
+  return cudaGetLastError();
 }
 
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st) {

@@ -152,14 +152,22 @@ def main():
                 run_case(cfg, 512, 256, 512, False, "int", torch.float32, 3, rank, world)
                 run_case(cfg, 512, 256, 512, False, "uniform", torch.bfloat16, 3, rank, world)
             ax.axonn_grid_finalize()
-        if rank == 0:   # fused (NVLS) and NCCL paths: bit-identical for 2-rank axes
+        if rank == 0:
+            # fused (NVLS) vs NCCL: bit-identical when every axis has <= 2 ranks
+            # (both compute RNE(a + b)); with 4-rank axes the fused owner phase
+            # rounds once where NCCL's ring rounds per hop -> compare to tolerance
+            exact = max(cfg[:2] + (cfg[3],)) <= 2
             for key, val in results.items():
                 if key[0] != "1":
                     continue
                 ref = results[("0",) + key[1:]]
                 for name, a, b in zip(("O", "dI", "dW"), val, ref):
-                    assert np.array_equal(a, b), f"fused != NCCL for {name} at {cfg} {key}"
-            print(f"fused==nccl bit-exact cfg={cfg}", flush=True)
+                    if exact:
+                        assert np.array_equal(a, b), f"fused != NCCL for {name} at {cfg} {key}"
+                    else:
+                        err = np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30)
+                        assert err <= 2e-2, f"fused vs NCCL {name} {err} at {cfg} {key}"
+            print(f"fused vs nccl {'bit-exact' if exact else 'within 2e-2'} cfg={cfg}", flush=True)
     dist.barrier()
     if rank == 0:
         print("MP_OK", flush=True)
