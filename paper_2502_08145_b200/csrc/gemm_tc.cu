@@ -62,6 +62,15 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n)
 
 __device__ __forceinline__ TileCoord tile_coord_g(int t, int tiles_m, int tiles_n, int group_m,
                                                   int bm, int bn) {
+  if (group_m < 0) {  // bands of -group_m N-tiles, M fastest... transposed raster
+    const int gn_sz = -group_m;
+    const int per_group = gn_sz * tiles_m;
+    const int g = t / per_group;
+    const int first_n = g * gn_sz;
+    const int gn = min(tiles_n - first_n, gn_sz);
+    const int r = t - g * per_group;
+    return {(r / gn) * bm, (first_n + r % gn) * bn};
+  }
   const int per_group = group_m * tiles_n;
   const int g = t / per_group;
   const int first_m = g * group_m;
@@ -241,37 +250,47 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 // ===================================================================== 2-CTA
 // CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
-// 256x256 tile.  Each CTA stages 128 rows of A and 128 rows (N) of B per
-// 64-wide K block (32 KiB per stage, 6 stages); the leader CTA issues
-// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads the peer's half
-// of A and B through the pair's shared operand path; each CTA's TMEM holds its
-// 128 rows of the fp32 accumulator (two 256-column buffers = all 512 columns).
-// Per tile and K block the pair moves 64 KiB from L2 instead of the 96 KiB two
-// independent 128x256 CTAs need.
-constexpr int P_BM = 256;                 // tile rows per pair (128 per CTA)
-constexpr int P_BN = 256;
-constexpr int P_STAGES = 6;
-constexpr int P_SMEM_A = 128 * BK * 2;    // 16 KiB per CTA
-constexpr int P_SMEM_B = 128 * BK * 2;    // 16 KiB per CTA (half of N)
-constexpr int P_STAGE_BYTES = P_SMEM_A + P_SMEM_B;
-constexpr int P_EPI_BYTES = 4 * 32 * 64 * 2;  // per epilogue warp: 32 rows x 64 bf16 staging
-constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + P_EPI_BYTES + 256;
+// (256*MT) x 256 tile; CTA r owns rows [r*128*MT, (r+1)*128*MT) of it.  Per
+// 64-wide K block each CTA stages its 128*MT rows of A and 128 rows (N/2) of
+// B; the leader issues MT tcgen05.mma.cta_group::2 (M=256, N=256, K=16) per
+// K=16 step — MMA mt reads rows [mt*128, mt*128+128) of both CTAs' A and both
+// halves of B — accumulating into TMEM columns [mt*256, mt*256+256).
+//   MT = 1: 256x256 tile, 6 stages of 32 KiB, two accumulators (the epilogue
+//           of tile i overlaps the main loop of tile i+1);
+//   MT = 2: 512x256 tile, 4 stages of 48 KiB, one accumulator filling all 512
+//           TMEM columns: 33% more flops per byte staged from L2 and a quarter
+//           fewer operand-panel reads per GEMM, which lowers L2/DRAM traffic
+//           and power (the B200 runs power-capped under this load).
+template <int MT>
+struct PairCfg {
+  static constexpr int ROWS_CTA = 128 * MT;
+  static constexpr int BM = 256 * MT;
+  static constexpr int BN = 256;
+  static constexpr int STAGES = MT == 1 ? 6 : 4;
+  static constexpr int ACC = 2 / MT;                // accumulator buffers in TMEM
+  static constexpr int SMEM_A = ROWS_CTA * BK * 2;
+  static constexpr int SMEM_B = 128 * BK * 2;
+  static constexpr int STAGE_BYTES = SMEM_A + SMEM_B;
+  static constexpr int EPI_BYTES = 4 * 32 * 64 * 2;  // per epilogue warp: 32 rows x 64 bf16
+  static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+};
 
-template <int A_MN, int B_MN>
+template <int A_MN, int B_MN, int MT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
                            int group_m, const __grid_constant__ EpiTarget epi) {
+  using Cfg = PairCfg<MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + P_STAGES * P_SMEM_A;
-  uint8_t* sEpi = sB + P_STAGES * P_SMEM_B;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + P_EPI_BYTES);
-  uint64_t* empty = full + P_STAGES;
-  uint64_t* tfull = empty + P_STAGES;
+  uint8_t* sB = smem + Cfg::STAGES * Cfg::SMEM_A;
+  uint8_t* sEpi = sB + Cfg::STAGES * Cfg::SMEM_B;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + Cfg::EPI_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -281,15 +300,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
-  const int tiles_m = (M + P_BM - 1) / P_BM;
-  const int tiles_n = (N + P_BN - 1) / P_BN;
+  const int tiles_m = (M + Cfg::BM - 1) / Cfg::BM;
+  const int tiles_n = (N + Cfg::BN - 1) / Cfg::BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    for (int s = 0; s < P_STAGES; ++s) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
@@ -311,20 +330,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster; t < num_tiles; t += nclusters) {
-        const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, P_BM, P_BN);
-        const int am = tc.m0 + 128 * static_cast<int>(rank);   // this CTA's A rows
-        const int bn = tc.n0 + 128 * static_cast<int>(rank);   // this CTA's half of N
+        const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
+        const int am = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank);  // this CTA's A rows
+        const int bn = tc.n0 + 128 * static_cast<int>(rank);            // this CTA's half of N
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
           const int k0 = kb * BK;
-          uint8_t* a_dst = sA + stage * P_SMEM_A;
-          uint8_t* b_dst = sB + stage * P_SMEM_B;
+          uint8_t* a_dst = sA + stage * Cfg::SMEM_A;
+          uint8_t* b_dst = sB + stage * Cfg::SMEM_B;
           if (A_MN == 0) {
-            ptx::tma_load_2d_2sm(a_dst, &tmA, &full[stage], k0, am);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)  // 128-row boxes, 16 KiB apart
+              ptx::tma_load_2d_2sm(a_dst + mt * 16384, &tmA, &full[stage], k0, am + 128 * mt);
           } else {
-            ptx::tma_load_2d_2sm(a_dst, &tmA, &full[stage], am, k0);
-            ptx::tma_load_2d_2sm(a_dst + MN_CHUNK_BYTES, &tmA, &full[stage], am + MN_CHUNK, k0);
+#pragma unroll
+            for (int c = 0; c < Cfg::ROWS_CTA / MN_CHUNK; ++c)
+              ptx::tma_load_2d_2sm(a_dst + c * MN_CHUNK_BYTES, &tmA, &full[stage],
+                                   am + c * MN_CHUNK, k0);
           }
           if (B_MN == 0) {
             ptx::tma_load_2d_2sm(b_dst, &tmB, &full[stage], k0, bn);
@@ -332,7 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             ptx::tma_load_2d_2sm(b_dst, &tmB, &full[stage], bn, k0);
             ptx::tma_load_2d_2sm(b_dst + MN_CHUNK_BYTES, &tmB, &full[stage], bn + MN_CHUNK, k0);
           }
-          if (++stage == P_STAGES) {
+          if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -342,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader only)
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(P_BM, P_BN, A_MN, B_MN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, Cfg::BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -350,36 +373,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int t = cluster; t < num_tiles; t += nclusters) {
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * P_BN);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * MT * Cfg::BN);
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_base = ptx::smem_u32(sA + stage * P_SMEM_A);
-          const uint32_t b_base = ptx::smem_u32(sB + stage * P_SMEM_B);
+          const uint32_t a_base = ptx::smem_u32(sA + stage * Cfg::SMEM_A);
+          const uint32_t b_base = ptx::smem_u32(sB + stage * Cfg::SMEM_B);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_base + kk * 2048, MN_CHUNK_BYTES, 1024)
-                                     : ptx::sdesc_sw128(a_base + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, MN_CHUNK_BYTES, 1024)
                                      : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
-            ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              // rows [mt*128, mt*128+128) of each CTA's A start 16 KiB apart in
+              // both majors (128 rows x 128 B, or two 8-KiB MN chunks)
+              const uint32_t ab = a_base + mt * 16384;
+              const uint64_t ad = A_MN ? ptx::sdesc_sw128(ab + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                       : ptx::sdesc_sw128(ab + kk * 32, 16, 1024);
+              ptx::umma_f16_2sm(d_tmem + mt * Cfg::BN, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
           }
           ptx::umma_commit_2sm(&empty[stage], 0x3);  // frees the slot in both CTAs
-          if (++stage == P_STAGES) {
+          if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::umma_commit_2sm(&tfull[acc], 0x3);      // both halves of the accumulator ready
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        ptx::umma_commit_2sm(&tfull[acc], 0x3);      // both CTAs' accumulators ready
+        if (++acc == Cfg::ACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (both CTAs)
     // TMEM -> registers (thread = row) -> bf16 -> XOR-swizzled smem -> 16-B
     // vectors with 8 consecutive threads covering one 128-B row segment, so
-    // every global store / NVLS reduction is a full line.
+    // every global store / NVLink write is a full line.
     const int e = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -387,77 +418,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint8_t* stage = sEpi + e * (32 * 64 * 2);
     const uint32_t stage_u32 = ptx::smem_u32(stage);
     for (int t = cluster; t < num_tiles; t += nclusters) {
-      const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, P_BM, P_BN);
+      const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = tc.m0 + 128 * static_cast<int>(rank) + 32 * e;
 #pragma unroll 1
-      for (int c = 0; c < P_BN / 64; ++c) {
+      for (int mt = 0; mt < MT; ++mt) {
+        const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
+        const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
+#pragma unroll 1
+        for (int c = 0; c < Cfg::BN / 64; ++c) {
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t v[32];
-          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) +
-                                 static_cast<uint32_t>(acc * P_BN + c * 64 + hh * 32);
-          ptx::tmem_ld_32x32b_x32(taddr, v);
-          ptx::tmem_wait_ld();
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
+                                   static_cast<uint32_t>(c * 64 + hh * 32);
+            ptx::tmem_ld_32x32b_x32(taddr, v);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int j = hh * 4 + q;  // 16-B unit of this row segment
-            const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                         "r"(ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1])),
-                         "r"(ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
-                         "r"(ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5])),
-                         "r"(ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
-                         : "memory");
+            for (int q = 0; q < 4; ++q) {
+              const int j = hh * 4 + q;  // 16-B unit of this row segment
+              const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                           "r"(ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1])),
+                           "r"(ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
+                           "r"(ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5])),
+                           "r"(ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
+                           : "memory");
+            }
           }
-        }
-        __syncwarp();
-        const int u = lane & 7;
-        const int gcol = tc.n0 + c * 64 + u * 8;
+          __syncwarp();
+          const int u = lane & 7;
+          const int gcol = tc.n0 + c * 64 + u * 8;
 #pragma unroll 2
-        for (int it = 0; it < 8; ++it) {
-          const int r = it * 4 + (lane >> 3);
-          uint4 w;
-          const uint32_t a = stage_u32 + r * 128 + ((u ^ (r & 7)) << 4);
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                       : "r"(a)
-                       : "memory");
-          const int grow = row0 + r;
-          if (grow < M && gcol < N) {
-            if (epi.mode == kMcRed) {
-              // fused 2-rank all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
-              ptx::multimem_red_add_bf16x8(epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2,
-                                           w);
-            } else if (epi.mode == kScatter) {
-              // fused reduce-scatter: this 16-B vector goes to its owner's slot
-              const long long f = static_cast<long long>(grow) * N + gcol;
-              const int o = static_cast<int>(f / epi.slice);
-              const long long off = static_cast<long long>(epi.me) * epi.slice + (f - o * epi.slice);
-              *reinterpret_cast<uint4*>(epi.peer[o] + static_cast<uint64_t>(off) * 2) = w;
-            } else if (vec_ok && gcol + 8 <= N) {
-              *reinterpret_cast<uint4*>(C + static_cast<int64_t>(grow) * ldc + gcol) = w;
-            } else {
-              const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-              __nv_bfloat16* dst = C + static_cast<int64_t>(grow) * ldc + gcol;
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + (lane >> 3);
+            uint4 w;
+            const uint32_t a = stage_u32 + r * 128 + ((u ^ (r & 7)) << 4);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                         : "r"(a)
+                         : "memory");
+            const int grow = row0 + r;
+            if (grow < M && gcol < N) {
+              if (epi.mode == kMcRed) {
+                // fused 2-rank all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
+                ptx::multimem_red_add_bf16x8(
+                    epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
+              } else if (epi.mode == kScatter) {
+                // fused reduce-scatter: this 16-B vector goes to its owner's slot
+                const long long f = static_cast<long long>(grow) * N + gcol;
+                const int o = static_cast<int>(f / epi.slice);
+                const long long off =
+                    static_cast<long long>(epi.me) * epi.slice + (f - o * epi.slice);
+                *reinterpret_cast<uint4*>(epi.peer[o] + static_cast<uint64_t>(off) * 2) = w;
+              } else if (vec_ok && gcol + 8 <= N) {
+                *reinterpret_cast<uint4*>(C + static_cast<int64_t>(grow) * ldc + gcol) = w;
+              } else {
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+                __nv_bfloat16* dst = C + static_cast<int64_t>(grow) * ldc + gcol;
 #pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                if (gcol + q < N) {
-                  const uint16_t bits = static_cast<uint16_t>(ws[q >> 1] >> (16 * (q & 1)));
-                  dst[q] = __ushort_as_bfloat16(bits);
+                for (int q = 0; q < 8; ++q) {
+                  if (gcol + q < N) {
+                    const uint16_t bits = static_cast<uint16_t>(ws[q >> 1] >> (16 * (q & 1)));
+                    dst[q] = __ushort_as_bfloat16(bits);
+                  }
                 }
               }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == Cfg::ACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
     if (epi.mode != kStore) ptx::fence_sys();  // remote writes performed before the kernel retires
   }
@@ -493,9 +531,17 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
   cuuint64_t strides[1] = {ld * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
+  static const int promo = [] {
+    const char* v = std::getenv("AXONN_L2_PROMOTION");  // 0 none, 1 64B, 2 128B, 3 256B
+    return v && *v ? std::atoi(v) : 3;
+  }();
+  const CUtensorMapL2promotion p =
+      promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+      : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+      : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, p,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -517,25 +563,34 @@ cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C,
   return cudaGetLastError();
 }
 
-template <int A_MN, int B_MN>
+template <int A_MN, int B_MN, int MT>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
                         int M, int N, int K, int num_sms, int group_m, const EpiTarget& epi,
                         cudaStream_t stream) {
-  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN>;
+  using Cfg = PairCfg<MT>;
+  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(P_SMEM_BYTES));
+                                         static_cast<int>(Cfg::SMEM_BYTES));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + P_BM - 1) / P_BM) * ((N + P_BN - 1) / P_BN);
+  const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + Cfg::BN - 1) / Cfg::BN);
   int grid = (num_sms / 2) * 2;
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
-  kern<<<grid, THREADS, P_SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
-                                                N, K, group_m, epi);
+  kern<<<grid, THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
+                                                  N, K, group_m, epi);
   return cudaGetLastError();
+}
+
+template <int A_MN, int B_MN>
+cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb, void* C,
+                           int64_t ldc, int M, int N, int K, int num_sms, int group_m,
+                           const EpiTarget& epi, cudaStream_t stream) {
+  return mt == 2 ? launch_pair<A_MN, B_MN, 2>(ma, mb, C, ldc, M, N, K, num_sms, group_m, epi, stream)
+                 : launch_pair<A_MN, B_MN, 1>(ma, mb, C, ldc, M, N, K, num_sms, group_m, epi, stream);
 }
 
 int env_int(const char* name, int dflt) {
@@ -547,7 +602,8 @@ int env_int(const char* name, int dflt) {
 
 // C[M][N] (bf16, ldc) = op(A) x op(B); see axonn_gemm in include/axonn.h.
 // AXONN_GEMM_VARIANT=single selects the 1-CTA kernel (kept for A/B timing);
-// the default is the CTA-pair kernel.  AXONN_GROUP_M sets the raster band.
+// the default is the CTA-pair kernel with a 256x256 tile (AXONN_PAIR_MT=2:
+// 512x256).  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
                         cudaStream_t stream, const EpiTarget* epi_in) {
@@ -560,6 +616,7 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
     return v && std::strcmp(v, "single") == 0;
   }();
   static const int group_m = env_int("AXONN_GROUP_M", 16);
+  static const int pair_mt = env_int("AXONN_PAIR_MT", 1) == 2 ? 2 : 1;
   CUtensorMap ma, mb;
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
   // B box rows along N: 256 for the single-CTA tile, 128 (half of N) per CTA of a pair.
@@ -589,9 +646,9 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
                   : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
   } else {
-    e = op == 0 ? launch_pair<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
-        : op == 1 ? launch_pair<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
-                  : launch_pair<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream);
+    e = op == 0 ? launch_pair_mt<0, 1>(pair_mt, ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
+        : op == 1 ? launch_pair_mt<0, 0>(pair_mt, ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
+                  : launch_pair_mt<1, 1>(pair_mt, ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream);
   }
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
 }
