@@ -293,6 +293,10 @@ struct axonn_fc {
   Fused fo;   // O   over the forward axis      (Alg. 1 line 4 fused into line 3)
   Fused fi;   // dI  over the backward axis     (line 12 fused into line 11)
   Fused fw;   // dŴ  over DATA when Gz == 1     (PAPER.md:313-317 fused into line 13)
+  Fused fz;   // RS_z fused into line 13: the epilogue scatters to the slice owners
+  axonn::SymBuf wstage;        // AG_z over copy engines: symmetric staging copy of Ŵ
+  std::vector<void*> wpeer;    // every Z rank's staging address (LSA)
+  cudaEvent_t ev_rsdone = nullptr;  // last fused RS_z finished reading its slots
 };
 
 namespace {
@@ -367,6 +371,24 @@ axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) 
   const size_t S_el = static_cast<size_t>(h->geo.what_len);
   CUDA_TRY(cudaEventRecord(h->ev_in, st));
   CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_in, 0));
+  if (h->wstage.ptr) {
+    // AG_z on the copy engines (no SMs): stage Ŵ in symmetric memory, then
+    // pull every rank's slice over NVLink into W_{j,i} in z order.
+    cudaStream_t zs = S.cstream[AX_Z];
+    const size_t bytes = S_el * elem_size(h->d.dtype);
+    STATUS_TRY(fused_barrier(AX_Z, zs));  // peers are done reading my previous staging
+    CUDA_TRY(cudaMemcpyAsync(h->wstage.ptr, W_hat, bytes, cudaMemcpyDeviceToDevice, zs));
+    STATUS_TRY(fused_barrier(AX_Z, zs));  // every rank's Ŵ is staged
+    for (int q = 0; q < S.g[AX_Z]; ++q) {
+      const void* src = q == S.c[AX_Z] ? W_hat : h->wpeer[q];
+      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(h->wbuf) + q * bytes, src, bytes,
+                               cudaMemcpyDeviceToDevice, zs));
+    }
+    count_comm(0, S.g[AX_Z], S_el, h->d.dtype);
+    CUDA_TRY(cudaEventRecord(h->ev_ag, zs));
+    h->prefetched = true;
+    return AXONN_OK;
+  }
   NCCL_TRY(ncclAllGather(W_hat, h->wbuf, S_el, nccl_type(h->d.dtype), S.axis_comm[AX_Z],
                          S.cstream[AX_Z]));
   count_comm(0, S.g[AX_Z], S_el, h->d.dtype);
@@ -485,8 +507,8 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
       S.sym_why[a].clear();
       if (g[a] > 8)
         S.sym_why[a] = "fused all-reduce implemented for up to 8 ranks";
-      else if (a == AX_Z || (a == AX_D && g[AX_Z] > 1))
-        S.sym_why[a] = "reduce-scatter / all-gather on this axis use NCCL";
+      else if (a == AX_D && g[AX_Z] > 1)
+        S.sym_why[a] = "data-parallel all-reduce after a Z reduce-scatter uses NCCL";
       else if (env_int("AXONN_FUSED", 1) == 0)
         S.sym_why[a] = "disabled by AXONN_FUSED=0";
       else
@@ -557,7 +579,8 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
     if (cudaMalloc(&h->wbuf, wbytes) != cudaSuccess || cudaMalloc(&h->dwpart, wbytes) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", 2 * wbytes));
   }
-  for (cudaEvent_t* e : {&h->ev_in, &h->ev_ag, &h->ev_ar, &h->ev_dw, &h->ev_rs, &h->ev_grad})
+  for (cudaEvent_t* e : {&h->ev_in, &h->ev_ag, &h->ev_ar, &h->ev_dw, &h->ev_rs, &h->ev_grad,
+                         &h->ev_rsdone})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
   if (desc->dtype == AXONN_BF16) {
@@ -566,6 +589,27 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
         !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, &why) ||
         (S.g[AX_Z] == 1 && !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, &why)))
       return cleanup(fail(AXONN_ERR_NCCL, "fused all-reduce buffers: %s", why.c_str()));
+  }
+  if (desc->dtype == AXONN_BF16 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
+      geo.what_len % 8 == 0 && geo.m_l > 0) {
+    std::string why;
+    const int P = S.g[AX_Z];
+    h->fz.axis = AX_Z;
+    h->fz.elems = static_cast<size_t>(geo.k_l * geo.n_l);
+    if (!axonn::sym_alloc(&S.sym[AX_Z], h->fz.elems * 2, &h->fz.recv, &why) ||
+        !axonn::sym_alloc(&S.sym[AX_Z], static_cast<size_t>(geo.what_len) * 2, &h->wstage, &why))
+      return cleanup(fail(AXONN_ERR_NCCL, "fused Z buffers: %s", why.c_str()));
+    h->fz.epi.mode = axonn::kScatter;
+    h->fz.epi.P = P;
+    h->fz.epi.me = S.c[AX_Z];
+    h->fz.epi.slice = geo.what_len;  // owner of flat index f is f / S = its Ŵ slice (R4)
+    h->wpeer.resize(P);
+    for (int q = 0; q < P; ++q) {
+      h->fz.epi.peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&h->fz.recv, q));
+      h->wpeer[q] = axonn::sym_peer_ptr(&h->wstage, q);
+      if (!h->fz.epi.peer[q] || !h->wpeer[q])
+        return cleanup(fail(AXONN_ERR_NCCL, "peer address of a Z window unavailable"));
+    }
   }
   h->ev_chunk.resize(h->d.chunks + 1, nullptr);
   for (auto& e : h->ev_chunk)
@@ -708,8 +752,9 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   const bool rs = S.g[AX_Z] > 1;
   const bool fI = h->fi.epi.mode != axonn::kStore;  // dI all-reduce fused into the dI GEMM
   const bool fW = h->fw.epi.mode != axonn::kStore;  // data-parallel dŴ all-reduce fused into the dW GEMM
+  const bool fZ = h->fz.epi.mode == axonn::kScatter;  // RS_z fused into the dW GEMM
   const size_t es = elem_size(dt);
-  void* dst = fW ? h->fw.out.ptr : (rs ? h->dwpart : dW_hat);
+  void* dst = fW ? h->fw.out.ptr : (rs && !fZ ? h->dwpart : dW_hat);
   const size_t S_el = static_cast<size_t>(g.what_len);
   cudaEvent_t last = nullptr;
   // line 11: dI^ = dO x W^T  (M = m_l, N = k_l, K = n_l)
@@ -719,12 +764,29 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   };
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
   auto dW_gemm = [&]() -> axonn_status_t {
+    if (fZ)  // the previous fused RS_z must have released every rank's slots
+      CUDA_TRY(cudaStreamWaitEvent(st, h->ev_rsdone, 0));
     return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
-                    st, fW ? &h->fw.epi : nullptr);
+                    st, fW ? &h->fw.epi : (fZ ? &h->fz.epi : nullptr));
   };
   // line 14 (ORS, waited in grads_sync) and the per-layer data-parallel sum
   auto grad_comm = [&]() -> axonn_status_t {
-    if (rs) {
+    if (rs && fZ) {
+      // fused RS_z, owner phase deferred on the Z stream (ORS): sum the Gz
+      // slots in rank order into this rank's Ŵ gradient slice
+      cudaStream_t zs = S.cstream[AX_Z];
+      CUDA_TRY(cudaEventRecord(h->ev_rs, st));
+      CUDA_TRY(cudaStreamWaitEvent(zs, h->ev_rs, 0));
+      STATUS_TRY(fused_barrier(AX_Z, zs));  // every rank's scatter has landed
+      CUDA_TRY(axonn::sym_owner_reduce(&h->fz.recv, nullptr, h->fz.epi.slice, h->fz.epi.P,
+                                       h->fz.epi.me, S.num_sms, zs, dW_hat));
+      g_launches.fetch_add(1);
+      STATUS_TRY(fused_barrier(AX_Z, zs));  // every owner is done with its slots
+      CUDA_TRY(cudaEventRecord(h->ev_rsdone, zs));
+      count_comm(1, S.g[AX_Z], S_el, dt);
+      CUDA_TRY(cudaEventRecord(h->ev_grad, zs));
+      last = h->ev_grad;
+    } else if (rs) {
       CUDA_TRY(cudaEventRecord(h->ev_rs, st));
       CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
       NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_Z],
@@ -805,7 +867,7 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
   if (!S.handles.count(h)) return fail(AXONN_ERR_ARG, "unknown handle");
   S.handles.erase(h);
   cudaDeviceSynchronize();
-  for (cudaEvent_t e : {h->ev_in, h->ev_ag, h->ev_ar, h->ev_dw, h->ev_rs, h->ev_grad}) {
+  for (cudaEvent_t e : {h->ev_in, h->ev_ag, h->ev_ar, h->ev_dw, h->ev_rs, h->ev_grad, h->ev_rsdone}) {
     if (!e) continue;
     for (size_t i = 0; i < S.pending_grads.size(); ++i)
       if (S.pending_grads[i] == e) S.pending_grads.erase(S.pending_grads.begin() + i--);
@@ -815,10 +877,11 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
     if (e) cudaEventDestroy(e);
   if (h->wbuf) cudaFree(h->wbuf);
   if (h->dwpart) cudaFree(h->dwpart);
-  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw}) {
+  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz}) {
     axonn::sym_free(&S.sym[f->axis], &f->out);
     axonn::sym_free(&S.sym[f->axis], &f->recv);
   }
+  axonn::sym_free(&S.sym[AX_Z], &h->wstage);
   delete h;
   return AXONN_OK;
 }

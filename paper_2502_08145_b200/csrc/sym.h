@@ -32,10 +32,11 @@ void sym_free(SymAxis* a, SymBuf* b);
 // 2 plain store to peer, 3 multimem.ld_reduce, 4 local store).
 void* sym_peer_ptr(SymBuf* b, int peer);
 cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms);
-// Owner phase of the P-rank fused all-reduce (see sym.cu): recv holds P slots
-// of `slice` bf16 elements; the sum goes to every rank's out[me*slice ...].
+// Owner phase of the P-rank fused all-reduce / reduce-scatter (see sym.cu):
+// recv holds P slots of `slice` bf16 elements; the sum goes to every rank's
+// out[me*slice ...] (multicast), or only to out_local when it is non-null.
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
-                             int me, int num_sms, cudaStream_t st);
+                             int me, int num_sms, cudaStream_t st, void* out_local = nullptr);
 // One-CTA cross-rank barrier on `st` (system-scope release/acquire).
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st);
 
