@@ -143,3 +143,20 @@ def test_full_size_sampled(op, M, N, K):
     got = C[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()].double().cpu().numpy()
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 2e-2
     assert np.all(np.abs(got - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-5 * np.sqrt(K))
+
+
+@pytest.mark.parametrize("env", [{"AXONN_GEMM_VARIANT": "single"}, {"AXONN_PAIR_MT": "2"},
+                                 {"AXONN_GROUP_M": "-8"}])
+def test_alternative_kernel_configurations(env):
+    """The 1-CTA kernel, the 512x256 CTA-pair tile and the transposed raster
+    (selected by environment, read once per process) pass the same bit-exact
+    integer and full-size checks."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(here, "test_gpu_gemm.py"), "-k",
+                        "integer or full_size or random"],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
