@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer
     if (lane == 0) {
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+    __syncwarp();
   } else if (warp >= 4) {
     // --------------------------------------------------------- epilogue
     const int e = warp - 4;  // TMEM lanes 32e .. 32e+31 (warp % 4 == e)
@@ -280,7 +282,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
-                           int group_m, const __grid_constant__ EpiTarget epi) {
+                           int group_m, const __grid_constant__ EpiTarget epi,
+                           int* __restrict__ tile_counter) {
   using Cfg = PairCfg<MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -292,7 +295,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tq_full = tempty + 2;     // tile queue (dynamic scheduling), both CTAs
+  uint64_t* tq_empty = tq_full + 4;   // consumer releases, counted on the leader
+  int* tq = reinterpret_cast<int*>(tq_empty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -304,6 +310,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int tiles_n = (N + Cfg::BN - 1) / Cfg::BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + BK - 1) / BK;
+  const bool dynamic = tile_counter != nullptr;
+
+  // Tile sequence.  Static: cluster c takes c, c + nclusters, ...  Dynamic:
+  // the leader's producer draws the next tile in raster order from a global
+  // counter when its cluster is ready for one, and publishes it to both CTAs'
+  // 4-entry queues; the other 10 consumers (peer producer, MMA, 4 + 4
+  // epilogue warps) read their own copy and release the slot on the leader.
+  // Keeping the tiles in flight a compact band of the raster keeps the
+  // operand panels they share resident in L2 across the whole K loop.
+  auto consume_tile = [&](int seq, bool arrive) -> int {
+    if (!dynamic) {
+      const int t = cluster + seq * nclusters;
+      return t < num_tiles ? t : -1;
+    }
+    const int slot = seq & 3;
+    ptx::mbar_wait_cluster(&tq_full[slot], (seq >> 2) & 1);
+    const int t = *reinterpret_cast<volatile int*>(&tq[slot]);
+    if (arrive) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_empty[slot]), 0));
+    return t;
+  };
+  auto produce_tile = [&](int seq) -> int {  // leader producer
+    if (!dynamic) {
+      const int t = cluster + seq * nclusters;
+      return t < num_tiles ? t : -1;
+    }
+    const int slot = seq & 3;
+    ptx::mbar_wait_cluster(&tq_empty[slot], ((seq >> 2) & 1) ^ 1);
+    int t = atomicAdd(tile_counter, 1);
+    if (t >= num_tiles) t = -1;
+    tq[slot] = t;
+    ptx::st_shared_cluster_u32(ptx::mapa_shared(ptx::smem_u32(&tq[slot]), 1), static_cast<uint32_t>(t));
+    ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_full[slot]), 0));
+    ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_full[slot]), 1));
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -315,6 +356,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    for (int q = 0; q < 4; ++q) {
+      ptx::mbar_init(&tq_full[q], 1);
+      ptx::mbar_init(&tq_empty[q], 10);
     }
     ptx::fence_mbar_init();
   }
@@ -329,7 +374,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      for (int seq = 0;; ++seq) {
+        const int t = leader ? produce_tile(seq) : consume_tile(seq, true);
+        if (t < 0) break;
         const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
         const int am = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank);  // this CTA's A rows
         const int bn = tc.n0 + 128 * static_cast<int>(rank);            // this CTA's half of N
@@ -362,6 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
     }
+    __syncwarp();  // lanes 1..31 park here (converged) until lane 0 is done
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader only)
     if (leader && lane == 0) {
@@ -370,7 +418,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      for (int seq = 0;; ++seq) {
+        if (consume_tile(seq, true) < 0) break;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * MT * Cfg::BN);
@@ -406,6 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
     }
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (both CTAs)
     // TMEM -> registers (thread = row) -> bf16 -> XOR-swizzled smem -> 16-B
@@ -417,7 +467,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
     uint8_t* stage = sEpi + e * (32 * 64 * 2);
     const uint32_t stage_u32 = ptx::smem_u32(stage);
-    for (int t = cluster; t < num_tiles; t += nclusters) {
+    for (int seq = 0;; ++seq) {
+      const int t = consume_tile(seq, false);
+      __syncwarp();
+      if (dynamic && lane == 0)
+        ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_empty[seq & 3]), 0));
+      if (t < 0) break;
       const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
@@ -563,6 +618,26 @@ cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C,
   return cudaGetLastError();
 }
 
+int env_int(const char* name, int dflt);
+
+// Dynamic tile scheduling: a ring of global counters, one zeroed per launch
+// (AXONN_SCHED=static disables it and returns nullptr).
+int* next_tile_counter(cudaStream_t stream) {
+  static const bool dyn = [] {
+    const char* v = std::getenv("AXONN_SCHED");
+    return !(v && std::strcmp(v, "static") == 0);
+  }();
+  if (!dyn) return nullptr;
+  constexpr int kSlots = 256;
+  static int* ring = nullptr;
+  static int next = 0;
+  if (!ring && cudaMalloc(&ring, kSlots * sizeof(int)) != cudaSuccess) return nullptr;
+  int* c = ring + next;
+  next = (next + 1) % kSlots;
+  if (cudaMemsetAsync(c, 0, sizeof(int), stream) != cudaSuccess) return nullptr;
+  return c;
+}
+
 template <int A_MN, int B_MN, int MT>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
                         int M, int N, int K, int num_sms, int group_m, const EpiTarget& epi,
@@ -580,8 +655,9 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, i
   int grid = (num_sms / 2) * 2;
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
+  int* counter = next_tile_counter(stream);
   kern<<<grid, THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
-                                                  N, K, group_m, epi);
+                                                  N, K, group_m, epi, counter);
   return cudaGetLastError();
 }
 
