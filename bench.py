@@ -460,7 +460,51 @@ def main():
         g1.record(stream)
         barrier()
         t_gemm = max_over_ranks(g0.elapsed_time(g1)) / args.steps
-        exposed = {"t_step_ms": t_ms, "t_gemm_only_ms": t_gemm,
+
+        # per layer: Alg. 1 forward / backward through the ABI vs the same
+        # local products alone (SURVEY.md §8(d) "per layer and per block")
+        names = ["qkv", "proj", "fc1", "fc2"]
+        nrep = max(3, min(args.steps, 20))
+        ev = {key: [torch.cuda.Event(enable_timing=True) for _ in range(2 * nrep)]
+              for key in [f"{n_}_{ph}" for n_ in names for ph in ("fwd", "bwd", "fwd_gemm", "bwd_gemm")]
+              + ["sync"]}
+        acc_ms = {key: 0.0 for key in ev}
+        for rep in range(nrep):
+            with torch.cuda.stream(stream):
+                for i, l in enumerate(L):
+                    ev[f"{names[i]}_fwd"][2 * rep].record(stream)
+                    ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], stream)
+                    ev[f"{names[i]}_fwd"][2 * rep + 1].record(stream)
+                    if i + 1 < len(L):
+                        ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
+                for i in reversed(range(len(L))):
+                    l = L[i]
+                    ev[f"{names[i]}_bwd"][2 * rep].record(stream)
+                    ax.axonn_fc_backward(l["h"], l["dO"], l["dI"], l["dW"], stream)
+                    ev[f"{names[i]}_bwd"][2 * rep + 1].record(stream)
+                ev["sync"][2 * rep].record(stream)
+                ax.axonn_grads_sync(stream)
+                ev["sync"][2 * rep + 1].record(stream)
+                for i, (l, (g, Wf, dWf)) in enumerate(zip(L, scratch)):
+                    ev[f"{names[i]}_fwd_gemm"][2 * rep].record(stream)
+                    ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, stream)
+                    ev[f"{names[i]}_fwd_gemm"][2 * rep + 1].record(stream)
+                    ev[f"{names[i]}_bwd_gemm"][2 * rep].record(stream)
+                    ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, stream)
+                    ax.axonn_gemm(2, 0, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, stream)
+                    ev[f"{names[i]}_bwd_gemm"][2 * rep + 1].record(stream)
+        barrier()
+        for key, lst in ev.items():
+            acc_ms[key] = max_over_ranks(sum(lst[2 * r].elapsed_time(lst[2 * r + 1])
+                                             for r in range(nrep)) / nrep)
+        per_layer = {}
+        for n_ in names:
+            for ph in ("fwd", "bwd"):
+                t_op, t_g = acc_ms[f"{n_}_{ph}"], acc_ms[f"{n_}_{ph}_gemm"]
+                per_layer[f"{n_}_{ph}"] = {"ms": t_op, "gemm_only_ms": t_g,
+                                           "exposed_frac": max(0.0, (t_op - t_g) / t_op) if t_op else 0.0}
+        per_layer["grads_sync"] = {"ms": acc_ms["sync"]}
+        exposed = {"t_step_ms": t_ms, "t_gemm_only_ms": t_gemm, "per_layer": per_layer,
                    "exposed_comm_frac": max(0.0, (t_ms - t_gemm) / t_ms),
                    "comm_bytes_per_rank_per_step": {k: v // max(1, args.steps + args.warmup)
                                                     for k, v in comm0.items()}}
