@@ -286,6 +286,7 @@ struct axonn_fc {
   struct Fused {
     int axis = 0;
     size_t elems = 0;
+    void* out_peer = nullptr;  // 2-rank scatter mode: the peer's copy of our slice
     axonn::SymBuf out;    // every rank's result (handle-owned output buffer)
     axonn::SymBuf recv;   // P-rank scatter mode: P slots of elems / P
     axonn::EpiTarget epi;
@@ -312,16 +313,24 @@ axonn_status_t fused_barrier(int axis, cudaStream_t st) {
 // commutative: bit-identical to NCCL); P >= 3: the epilogue scatters 16-B
 // vectors to their owner rank, the owner sums the P slots in rank order and
 // multicasts the result (every element reduced once: replicas bit-identical).
-bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, std::string* why) {
+// `kdim` is the contraction length of the producing GEMM: its output leaves the
+// epilogue at ~(GEMM flop rate)/K bytes/s.  2-rank axes use multimem.red when
+// that rate stays well inside what NVLS reductions sustain from the epilogue
+// (K >= AXONN_RED_MIN_K, default 8192): fully overlapped, no extra pass.
+// Shorter K (e.g. the transposed proj layer, K = h/Gx) uses the scatter mode,
+// whose epilogue traffic is half as large and goes out as plain stores.
+bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_t kdim,
+                 std::string* why) {
   f->axis = axis;
   f->epi = axonn::EpiTarget();
   const int P = S.g[axis];
   const int64_t n = rows * cols;
   if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % 8) return true;  // NCCL path
-  if (P > 2 && n % (8 * P)) return true;
+  const bool red = P == 2 && kdim >= env_int("AXONN_RED_MIN_K", 8192);
+  if (!red && n % (8 * P)) return true;
   f->elems = static_cast<size_t>(n);
   if (!axonn::sym_alloc(&S.sym[axis], f->elems * 2, &f->out, why)) return false;
-  if (P == 2) {
+  if (red) {
     f->epi.mode = axonn::kMcRed;
     f->epi.mc = reinterpret_cast<unsigned long long>(f->out.mc);
     return true;
@@ -337,6 +346,14 @@ bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, std::
       *why = "peer address of the receive window unavailable";
       return false;
     }
+  }
+  if (P == 2) {  // the owner sends its reduced slice to the peer with plain stores
+    char* peer_out = static_cast<char*>(axonn::sym_peer_ptr(&f->out, 1 - f->epi.me));
+    if (!peer_out) {
+      *why = "peer address of the output window unavailable";
+      return false;
+    }
+    f->out_peer = peer_out + static_cast<size_t>(f->epi.me) * f->epi.slice * 2;
   }
   return true;
 }
@@ -355,8 +372,11 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
 axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st) {
   STATUS_TRY(fused_barrier(f.axis, st));  // every rank's epilogue writes have landed
   if (f.epi.mode == axonn::kScatter) {
+    void* local = nullptr;
+    if (f.out_peer)  // 2 ranks: own copy + plain stores to the peer instead of multicast
+      local = static_cast<char*>(f.out.ptr) + static_cast<size_t>(f.epi.me) * f.epi.slice * 2;
     CUDA_TRY(axonn::sym_owner_reduce(&f.recv, &f.out, f.epi.slice, f.epi.P, f.epi.me, S.num_sms,
-                                     st));
+                                     st, local, f.out_peer));
     g_launches.fetch_add(1);
     STATUS_TRY(fused_barrier(f.axis, st));  // every owner's broadcast has landed
   }
@@ -585,9 +605,9 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
   if (desc->dtype == AXONN_BF16) {
     std::string why;
-    if (!fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, &why) ||
-        !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, &why) ||
-        (S.g[AX_Z] == 1 && !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, &why)))
+    if (!fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, &why) ||
+        !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, &why) ||
+        (S.g[AX_Z] == 1 && !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why)))
       return cleanup(fail(AXONN_ERR_NCCL, "fused all-reduce buffers: %s", why.c_str()));
   }
   if (desc->dtype == AXONN_BF16 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&

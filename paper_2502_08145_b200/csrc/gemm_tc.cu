@@ -257,9 +257,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 // B; the leader issues MT tcgen05.mma.cta_group::2 (M=256, N=256, K=16) per
 // K=16 step — MMA mt reads rows [mt*128, mt*128+128) of both CTAs' A and both
 // halves of B — accumulating into TMEM columns [mt*256, mt*256+256).
-//   MT = 1: 256x256 tile, 6 stages of 32 KiB, two accumulators (the epilogue
+//   MT = 1: 256x256 tile, 5 stages of 32 KiB, two accumulators (the epilogue
 //           of tile i overlaps the main loop of tile i+1);
-//   MT = 2: 512x256 tile, 4 stages of 48 KiB, one accumulator filling all 512
+//   MT = 2: 512x256 tile, 3 stages of 48 KiB, one accumulator filling all 512
 //           TMEM columns: 33% more flops per byte staged from L2 and a quarter
 //           fewer operand-panel reads per GEMM, which lowers L2/DRAM traffic
 //           and power (the B200 runs power-capped under this load).
@@ -268,17 +268,19 @@ struct PairCfg {
   static constexpr int ROWS_CTA = 128 * MT;
   static constexpr int BM = 256 * MT;
   static constexpr int BN = 256;
-  static constexpr int STAGES = MT == 1 ? 6 : 4;
+  static constexpr int STAGES = MT == 1 ? 5 : 3;
   static constexpr int ACC = 2 / MT;                // accumulator buffers in TMEM
   static constexpr int SMEM_A = ROWS_CTA * BK * 2;
   static constexpr int SMEM_B = 128 * BK * 2;
   static constexpr int STAGE_BYTES = SMEM_A + SMEM_B;
-  static constexpr int EPI_BYTES = 4 * 32 * 64 * 2;  // per epilogue warp: 32 rows x 64 bf16
+  static constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each owning half the columns
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 64 * 2;  // per warp: 32 rows x 64 bf16
   static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
 template <int A_MN, int B_MN, int MT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
@@ -315,8 +317,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   // Tile sequence.  Static: cluster c takes c, c + nclusters, ...  Dynamic:
   // the leader's producer draws the next tile in raster order from a global
   // counter when its cluster is ready for one, and publishes it to both CTAs'
-  // 4-entry queues; the other 10 consumers (peer producer, MMA, 4 + 4
-  // epilogue warps) read their own copy and release the slot on the leader.
+  // 4-entry queues; the other consumers (peer producer, MMA, every epilogue
+  // warp of both CTAs) read their own copy and release the slot on the leader.
   // Keeping the tiles in flight a compact band of the raster keeps the
   // operand panels they share resident in L2 across the whole K loop.
   auto consume_tile = [&](int seq, bool arrive) -> int {
@@ -355,11 +357,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+      ptx::mbar_init(&tempty[a], 2 * Cfg::EPI_WARPS);  // every epilogue warp of the pair
     }
     for (int q = 0; q < 4; ++q) {
       ptx::mbar_init(&tq_full[q], 1);
-      ptx::mbar_init(&tq_empty[q], 10);
+      ptx::mbar_init(&tq_empty[q], 2 + 2 * Cfg::EPI_WARPS);  // MMA, peer producer, epilogues
     }
     ptx::fence_mbar_init();
   }
@@ -461,11 +463,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // TMEM -> registers (thread = row) -> bf16 -> XOR-swizzled smem -> 16-B
     // vectors with 8 consecutive threads covering one 128-B row segment, so
     // every global store / NVLink write is a full line.
-    const int e = warp - 4;
+    const int ew = warp - 4;          // epilogue warp 0..7
+    const int e = ew & 3;             // TMEM lane quarter (warp % 4)
+    const int chalf = ew >> 2;        // which 128 columns of the tile this warp stores
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
-    uint8_t* stage = sEpi + e * (32 * 64 * 2);
+    uint8_t* stage = sEpi + ew * (32 * 64 * 2);
     const uint32_t stage_u32 = ptx::smem_u32(stage);
     for (int seq = 0;; ++seq) {
       const int t = consume_tile(seq, false);
@@ -481,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
         const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
 #pragma unroll 1
-        for (int c = 0; c < Cfg::BN / 64; ++c) {
+        for (int c = chalf * 2; c < chalf * 2 + 2; ++c) {
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t v[32];
@@ -656,8 +660,8 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, i
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
   int* counter = next_tile_counter(stream);
-  kern<<<grid, THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc, M,
-                                                  N, K, group_m, epi, counter);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc,
+                                                       M, N, K, group_m, epi, counter);
   return cudaGetLastError();
 }
 

@@ -64,7 +64,8 @@ __global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
 // broadcast the result into every rank's output copy with multimem.st.  Every
 // element is reduced by exactly one rank, so all replicas hold the same bits.
 __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, int P,
-                               unsigned long long out_mc, uint4* __restrict__ out_local) {
+                               unsigned long long out_mc, uint4* __restrict__ out_local,
+                               uint4* __restrict__ out_peer) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n16;
        i += stride) {
@@ -84,8 +85,9 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, in
       __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
       o[q] = *reinterpret_cast<uint32_t*>(&h);
     }
-    if (out_local) {  // reduce-scatter: the owner keeps its slice
+    if (out_local) {  // reduce-scatter: the owner keeps its slice ...
       out_local[i] = make_uint4(o[0], o[1], o[2], o[3]);
+      if (out_peer) out_peer[i] = make_uint4(o[0], o[1], o[2], o[3]);  // ... 2 ranks: and sends it
     } else {
       asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
                        out_mc + static_cast<unsigned long long>(i) * 16),
@@ -228,7 +230,8 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
 }
 
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
-                             int me, int num_sms, cudaStream_t st, void* out_local) {
+                             int me, int num_sms, cudaStream_t st, void* out_local,
+                             void* out_peer) {
   const long long n16 = slice / 8;
   long long blocks = (n16 + 255) / 256;
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
@@ -238,7 +241,8 @@ cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long sl
                 : reinterpret_cast<unsigned long long>(out->mc) +
                       static_cast<unsigned long long>(me) * slice * 2;
   k_owner_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-      reinterpret_cast<const uint4*>(recv->ptr), n16, P, mc, static_cast<uint4*>(out_local));
+      reinterpret_cast<const uint4*>(recv->ptr), n16, P, mc, static_cast<uint4*>(out_local),
+      static_cast<uint4*>(out_peer));
   return cudaGetLastError();
 }
 

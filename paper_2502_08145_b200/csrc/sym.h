@@ -34,9 +34,11 @@ void* sym_peer_ptr(SymBuf* b, int peer);
 cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms);
 // Owner phase of the P-rank fused all-reduce / reduce-scatter (see sym.cu):
 // recv holds P slots of `slice` bf16 elements; the sum goes to every rank's
-// out[me*slice ...] (multicast), or only to out_local when it is non-null.
+// out[me*slice ...] (multicast), or to out_local when it is non-null (and also
+// to out_peer with plain NVLink stores when that is non-null: 2-rank axes).
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
-                             int me, int num_sms, cudaStream_t st, void* out_local = nullptr);
+                             int me, int num_sms, cudaStream_t st, void* out_local = nullptr,
+                             void* out_peer = nullptr);
 // One-CTA cross-rank barrier on `st` (system-scope release/acquire).
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st);
 

@@ -128,10 +128,13 @@ def main():
     shapes = [(256, 512, 1024), (384, 192, 320)]
     for cfg in ogrid.enumerate_configs(world):
         results = {}
-        for fused in ("1", "0"):
-            os.environ["AXONN_FUSED"] = fused
+        # "red": 2-rank axes reduce with multimem.red; "scatter": 2-rank axes use
+        # the scatter + owner phase; "0": NCCL collectives (AXONN_FUSED=0)
+        for fused in ("red", "scatter", "0"):
+            os.environ["AXONN_FUSED"] = "0" if fused == "0" else "1"
+            os.environ["AXONN_RED_MIN_K"] = "0" if fused == "red" else str(1 << 30)
             ax.axonn_grid_init(*cfg)
-            if fused == "1" and rank == 0:
+            if fused == "red" and rank == 0:
                 print(f"cfg={cfg} fused status:",
                       {a: ax.axonn_fused_status(a) for a in "xyzd"}, flush=True)
             for (m, k, n) in shapes:
@@ -142,7 +145,7 @@ def main():
                         run_case(cfg, m, k, n, transposed, "int", torch.float32, 1, rank, world)
                     results[(fused, m, k, n, transposed)] = run_case(
                         cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank, world)
-                    if fused == "1":
+                    if fused == "red":
                         zc = run_case(cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank,
                                       world, zero_copy=True)
                         if rank == 0:
@@ -158,7 +161,7 @@ def main():
             # rounds once where NCCL's ring rounds per hop -> compare to tolerance
             exact = max(cfg) <= 2
             for key, val in results.items():
-                if key[0] != "1":
+                if key[0] == "0":
                     continue
                 ref = results[("0",) + key[1:]]
                 for name, a, b in zip(("O", "dI", "dW"), val, ref):
