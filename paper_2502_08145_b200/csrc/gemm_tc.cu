@@ -682,8 +682,9 @@ int env_int(const char* name, int dflt) {
 
 // C[M][N] (bf16, ldc) = op(A) x op(B); see axonn_gemm in include/axonn.h.
 // AXONN_GEMM_VARIANT=single selects the 1-CTA kernel (kept for A/B timing);
-// the default is the CTA-pair kernel with a 256x256 tile (AXONN_PAIR_MT=2:
-// 512x256).  AXONN_GROUP_M sets the raster band.
+// the default is the CTA-pair kernel: 512x256 tiles for plain launches
+// (AXONN_PAIR_MT=1: 256x256), 256x256 for fused-collective epilogues
+// (AXONN_PAIR_MT_FUSED=2: 512x256).  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
                         cudaStream_t stream, const EpiTarget* epi_in) {
@@ -696,7 +697,11 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
     return v && std::strcmp(v, "single") == 0;
   }();
   static const int group_m = env_int("AXONN_GROUP_M", 16);
-  static const int pair_mt = env_int("AXONN_PAIR_MT", 1) == 2 ? 2 : 1;
+  // 512x256 tiles (MT=2: less L2/DRAM traffic per flop) for plain-store
+  // launches; 256x256 (MT=1: double-buffered TMEM, so the NVLink-writing
+  // epilogue overlaps the next tile's main loop) for fused-collective epilogues.
+  static const int mt_plain = env_int("AXONN_PAIR_MT", 2) == 1 ? 1 : 2;
+  static const int mt_fused = env_int("AXONN_PAIR_MT_FUSED", 1) == 2 ? 2 : 1;
   CUtensorMap ma, mb;
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
   // B box rows along N: 256 for the single-CTA tile, 128 (half of N) per CTA of a pair.
@@ -721,6 +726,7 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode != kStore && (single || (N & 7) || (ldc & 7))) return GemmStatus::kBadAlignment;
   if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
+  const int pair_mt = epi.mode == kStore ? mt_plain : mt_fused;
   if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)

@@ -145,12 +145,12 @@ def test_full_size_sampled(op, M, N, K):
     assert np.all(np.abs(got - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-5 * np.sqrt(K))
 
 
-@pytest.mark.parametrize("env", [{"AXONN_GEMM_VARIANT": "single"}, {"AXONN_PAIR_MT": "2"},
-                                 {"AXONN_GROUP_M": "-8"}])
+@pytest.mark.parametrize("env", [{"AXONN_GEMM_VARIANT": "single"}, {"AXONN_PAIR_MT": "1"},
+                                 {"AXONN_GROUP_M": "-8"}, {"AXONN_SCHED": "static"}])
 def test_alternative_kernel_configurations(env):
-    """The 1-CTA kernel, the 512x256 CTA-pair tile and the transposed raster
-    (selected by environment, read once per process) pass the same bit-exact
-    integer and full-size checks."""
+    """The 1-CTA kernel, the 256x256 CTA-pair tile, the transposed raster and
+    static tile scheduling (selected by environment, read once per process)
+    pass the same bit-exact integer and full-size checks."""
     import os
     import subprocess
     import sys
