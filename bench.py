@@ -207,13 +207,13 @@ def run_reference(args):
     emit(out)
 
 
-def workload_config(model, n, grid):
+def workload_config(model, n, grid, tpg=16384):
     h = HIDDEN[model]
     return {"workload": (f"GPT-{model} block FC layers (QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h; "
-                         f"h={h}) Alg. 1 fwd+bwd, 16384 tokens per GPU"
-                         + (" (BASELINE.json configs[1], C2)" if n == 1 and model == "5B" else
-                            f", global m={16384 * n}")),
-            "grid": list(grid) if grid else None, "tokens": 16384 * n, "hidden": h,
+                         f"h={h}) Alg. 1 fwd+bwd, {tpg} tokens per GPU"
+                         + (" (BASELINE.json configs[1], C2)" if n == 1 and model == "5B" and tpg == 16384
+                            else f", global m={tpg * n}")),
+            "grid": list(grid) if grid else [1, 1, 1, 1], "tokens": tpg * n, "hidden": h,
             "phase": "A (proj, fc2 transposed)",
             "l2": "no flush: per-step operands (>= 134 MB each for I/dO of the fc2 layer) exceed the 126 MB L2"}
 
@@ -227,6 +227,8 @@ def main():
     ap.add_argument("--impl", default="axonn", choices=["axonn", "reference"])
     ap.add_argument("--grid", default=None, help="gx,gy,gz,gd (default: model-selected)")
     ap.add_argument("--model", default="5B", choices=sorted(HIDDEN))
+    ap.add_argument("--tokens-per-gpu", type=int, default=16384,
+                    help="global m = tokens-per-gpu x N (BASELINE.json: 16384)")
     ap.add_argument("--chunks", type=int, default=4, help="forward AR pipelining chunks")
     ap.add_argument("--gemm-sms", type=int, default=0, help="SM budget of the GEMM grid (0 = all)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -255,7 +257,7 @@ def main():
     import paper_2502_08145_b200 as ax
 
     h = HIDDEN[args.model]
-    m = 16384 * world
+    m = args.tokens_per_gpu * world
     layers = block_layers(h, m)
     if args.grid:
         grid = tuple(int(x) for x in args.grid.split(","))
@@ -520,7 +522,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (uniform(-1,1) bf16, device-generated, seeded)",
-            "config": workload_config(args.model, world, grid),
+            "config": workload_config(args.model, world, grid, args.tokens_per_gpu),
             "per_gpu_tflops": value / world,
             "frac_of_peak": {"advertised_2250": value / world / 2250.0,
                              "measured_burst": value / world / burst,
