@@ -232,6 +232,8 @@ def main():
     ap.add_argument("--chunks", type=int, default=4, help="forward AR pipelining chunks")
     ap.add_argument("--gemm-sms", type=int, default=0, help="SM budget of the GEMM grid (0 = all)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one step in a CUDA graph and time its replays")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     # Exactly one JSON line on stdout: libraries (NCCL prints its version line)
@@ -326,21 +328,44 @@ def main():
 
     # ---------------------------------------------------------------- timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph = None
+    if args.graph:
+        # one whole step (every kernel, NCCL call, barrier, copy, cross-stream
+        # event) captured once; profiling events inside it report the last replay
+        ax.axonn_profile_read()
+        ax.axonn_profile_enable(True)
+        launches0 = ax.axonn_kernel_launches()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
+            step(stream)
+        ax.axonn_profile_enable(False)
+        per_step_launches = ax.axonn_kernel_launches() - launches0
+        for _ in range(2):
+            graph.replay()
+        barrier()
     launches0 = ax.axonn_kernel_launches()
-    ax.axonn_profile_read()
-    ax.axonn_profile_enable(True)
+    if not args.graph:
+        ax.axonn_profile_read()
+        ax.axonn_profile_enable(True)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
         with torch.cuda.stream(stream):
             for _ in range(args.steps):
-                step(stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step(stream)
         ev1.record(stream)
         barrier()
     ax.axonn_profile_enable(False)
     launches = ax.axonn_kernel_launches() - launches0
+    if graph is not None:
+        launches = per_step_launches * args.steps
     comm0 = ax.axonn_comm_bytes(reset=True)
     gemm_n, gemm_ms, gemm_flops = ax.axonn_profile_read()
+    if graph is not None:  # events captured once hold the last replay: one step
+        gemm_n, gemm_ms, gemm_flops = gemm_n * args.steps, gemm_ms * args.steps, gemm_flops * args.steps
     t_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     flops_step = model_flops(layers)              # whole job (all ranks)
     value = flops_step / (t_ms * 1e-3) / 1e12
@@ -535,6 +560,7 @@ def main():
                          "peak_kind": f"bf16_tflops_sustained, {peaks_src}",
                          "frac_of_burst": achieved / burst if burst else None,
                          "gemm_launches": gemm_n, "gemm_ms_per_step": gemm_ms / args.steps},
+            "cuda_graph": bool(args.graph),
             "gpu_launches": launches,
             "overlap": exposed,
             "clocks": clk.summary(),

@@ -173,6 +173,15 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
     return AXONN_OK;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // Inside a CUDA-graph capture a plain event record is only a dependency
+  // marker; timing events must become external event-record nodes.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (S.profiling) CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+  auto record = [&](cudaEvent_t e) {
+    return cap == cudaStreamCaptureStatusActive
+               ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+               : cudaEventRecord(e, st);
+  };
   if (S.profiling) {
     for (cudaEvent_t* e : {&e0, &e1}) {
       if (!S.prof_free.empty()) {
@@ -182,7 +191,7 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
         CUDA_TRY(cudaEventCreate(e));
       }
     }
-    CUDA_TRY(cudaEventRecord(e0, st));
+    CUDA_TRY(record(e0));
   }
   axonn::GemmStatus gs;
   if (dtype == AXONN_BF16)
@@ -207,7 +216,7 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
   }
   g_launches.fetch_add(1);
   if (S.profiling) {
-    CUDA_TRY(cudaEventRecord(e1, st));
+    CUDA_TRY(record(e1));
     S.prof.push_back({e0, e1, 2.0 * static_cast<double>(M) * N * K});
   }
   return AXONN_OK;

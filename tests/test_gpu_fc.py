@@ -86,3 +86,35 @@ def test_kernel_launch_counter_and_profile(ax):
     launches, ms, flops = ax.axonn_profile_read()
     assert ax.axonn_kernel_launches() - n0 == 3 == launches
     assert flops == 3 * 2 * 256 ** 3 and ms > 0
+
+
+def test_cuda_graph_capture_and_replay(ax):
+    """Alg. 1 forward + backward + grads_sync captured in one CUDA graph and
+    replayed on fresh inputs gives the oracle's results (integer inputs, exact)."""
+    torch = require_cuda()
+    m, k, n = 384, 256, 520
+    h = ax.axonn_fc_create(m, k, n, False, ax.AXONN_BF16)
+    bufs = {name: torch.zeros(shape, dtype=torch.bfloat16, device="cuda") for name, shape in
+            (("I", (m, k)), ("W", (k * n,)), ("dO", (m, n)), ("O", (m, n)), ("dI", (m, k)),
+             ("dW", (k * n,)))}
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):   # warm-up (first-launch attribute setup happens here)
+        ax.axonn_fc_forward(h, bufs["I"], bufs["W"], bufs["O"], s)
+        ax.axonn_fc_backward(h, bufs["dO"], bufs["dI"], bufs["dW"], s)
+        ax.axonn_grads_sync(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        ax.axonn_fc_forward(h, bufs["I"], bufs["W"], bufs["O"], s)
+        ax.axonn_fc_backward(h, bufs["dO"], bufs["dI"], bufs["dW"], s)
+        ax.axonn_grads_sync(s)
+    for seed in (5, 6):
+        X, W, dY = synthdata.layer_tensors(m, k, n, seed, kind="int")
+        bufs["I"].copy_(to_dev(X, torch.bfloat16))
+        bufs["W"].copy_(to_dev(W, torch.bfloat16).reshape(-1))
+        bufs["dO"].copy_(to_dev(dY, torch.bfloat16))
+        g.replay()
+        torch.cuda.synchronize()
+        for got, ref in zip((bufs["O"], bufs["dI"], bufs["dW"].reshape(k, n)), fc.fc_layer(X, W, dY)):
+            assert np.array_equal(bf16_bits_of(got), synthdata.bf16_bits(synthdata.bf16_round(ref)))
+    ax.axonn_fc_destroy(h)
