@@ -696,7 +696,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
     const char* v = std::getenv("AXONN_GEMM_VARIANT");
     return v && std::strcmp(v, "single") == 0;
   }();
-  static const int group_m = env_int("AXONN_GROUP_M", 16);
+  // raster band: 4096 rows of tiles (AXONN_GROUP_M overrides, in tiles; < 0 = bands of N tiles)
+  static const int group_m_env = env_int("AXONN_GROUP_M", 0);
   // 512x256 tiles (MT=2: less L2/DRAM traffic per flop) for plain-store
   // launches; 256x256 (MT=1: double-buffered TMEM, so the NVLink-writing
   // epilogue overlaps the next tile's main loop) for fused-collective epilogues.
@@ -727,6 +728,7 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   const int pair_mt = epi.mode == kStore ? mt_plain : mt_fused;
+  const int group_m = group_m_env != 0 ? group_m_env : (single ? 32 : 16 / pair_mt);
   if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
