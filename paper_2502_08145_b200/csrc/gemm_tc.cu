@@ -283,6 +283,7 @@ template <int A_MN, int B_MN, int MT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmC, int use_tma_store,
                            __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
                            int group_m, const __grid_constant__ EpiTarget epi,
                            int* __restrict__ tile_counter) {
@@ -351,6 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if (use_tma_store) ptx::prefetch_tmap(&tmC);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -505,6 +507,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                            : "memory");
             }
           }
+          if (use_tma_store && epi.mode == kStore) {
+            // the staged chunk is exactly TMA's 128-B-swizzled 32 x 64 box
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmC, stage, tc.n0 + c * 64, row0);
+              ptx::tma_store_commit();
+              ptx::tma_store_wait_read();  // staging buffer reusable
+            }
+            __syncwarp();
+            continue;
+          }
           __syncwarp();
           const int u = lane & 7;
           const int gcol = tc.n0 + c * 64 + u * 8;
@@ -557,6 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
       }
     }
     if (epi.mode != kStore) ptx::fence_sys();  // remote writes performed before the kernel retires
+    if (use_tma_store && lane == 0) ptx::tma_store_wait_all();
   }
 
   ptx::tc_fence_before();
@@ -643,9 +658,9 @@ int* next_tile_counter(cudaStream_t stream) {
 }
 
 template <int A_MN, int B_MN, int MT>
-cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc,
-                        int M, int N, int K, int num_sms, int group_m, const EpiTarget& epi,
-                        cudaStream_t stream) {
+cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                        int use_tma_store, void* C, int64_t ldc, int M, int N, int K, int num_sms,
+                        int group_m, const EpiTarget& epi, cudaStream_t stream) {
   using Cfg = PairCfg<MT>;
   auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT>;
   static bool attr_set = false;
@@ -660,17 +675,21 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, i
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
   int* counter = next_tile_counter(stream);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, static_cast<__nv_bfloat16*>(C), ldc,
-                                                       M, N, K, group_m, epi, counter);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, mc, use_tma_store,
+                                                       static_cast<__nv_bfloat16*>(C), ldc, M, N, K,
+                                                       group_m, epi, counter);
   return cudaGetLastError();
 }
 
 template <int A_MN, int B_MN>
-cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb, void* C,
-                           int64_t ldc, int M, int N, int K, int num_sms, int group_m,
-                           const EpiTarget& epi, cudaStream_t stream) {
-  return mt == 2 ? launch_pair<A_MN, B_MN, 2>(ma, mb, C, ldc, M, N, K, num_sms, group_m, epi, stream)
-                 : launch_pair<A_MN, B_MN, 1>(ma, mb, C, ldc, M, N, K, num_sms, group_m, epi, stream);
+cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb,
+                           const CUtensorMap& mc, int use_tma_store, void* C, int64_t ldc, int M,
+                           int N, int K, int num_sms, int group_m, const EpiTarget& epi,
+                           cudaStream_t stream) {
+  return mt == 2 ? launch_pair<A_MN, B_MN, 2>(ma, mb, mc, use_tma_store, C, ldc, M, N, K, num_sms,
+                                             group_m, epi, stream)
+                 : launch_pair<A_MN, B_MN, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K, num_sms,
+                                             group_m, epi, stream);
 }
 
 int env_int(const char* name, int dflt) {
@@ -728,15 +747,25 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   const int pair_mt = epi.mode == kStore ? mt_plain : mt_fused;
+  // TMA-store epilogue for plain launches when C satisfies TMA's alignment
+  // (16-byte base and row pitch); AXONN_TMA_STORE=0 keeps per-thread stores.
+  static const bool tma_store_env = env_int("AXONN_TMA_STORE", 1) != 0;
+  CUtensorMap mc;
+  int use_tma_store = 0;
+  if (!single && epi.mode == kStore && tma_store_env && (ldc & 7) == 0 &&
+      (reinterpret_cast<uintptr_t>(C) & 15) == 0 && make_map(&mc, C, N, M, ldc, 64, 32))
+    use_tma_store = 1;
+  else
+    std::memset(&mc, 0, sizeof mc);
   const int group_m = group_m_env != 0 ? group_m_env : (single ? 32 : 16 / pair_mt);
   if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
                   : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
   } else {
-    e = op == 0 ? launch_pair_mt<0, 1>(pair_mt, ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
-        : op == 1 ? launch_pair_mt<0, 0>(pair_mt, ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream)
-                  : launch_pair_mt<1, 1>(pair_mt, ma, mb, C, ldc, m, n, k, num_sms, group_m, epi, stream);
+    e = op == 0 ? launch_pair_mt<0, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream)
+        : op == 1 ? launch_pair_mt<0, 0>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream)
+                  : launch_pair_mt<1, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream);
   }
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
 }
