@@ -746,7 +746,11 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode != kStore && (single || (N & 7) || (ldc & 7))) return GemmStatus::kBadAlignment;
   if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
-  const int pair_mt = epi.mode == kStore ? mt_plain : mt_fused;
+  // MT=2's single accumulator serialises the epilogue with the next tile; on
+  // short K loops that costs more than its lower L2/DRAM traffic saves
+  // (AXONN_MT2_MIN_K: smallest K that takes the 512x256 tile).
+  static const int mt2_min_k = env_int("AXONN_MT2_MIN_K", 0);
+  const int pair_mt = epi.mode != kStore ? mt_fused : (K >= mt2_min_k ? mt_plain : 1);
   // TMA-store epilogue for plain launches when C satisfies TMA's alignment
   // (16-byte base and row pitch); AXONN_TMA_STORE=0 keeps per-thread stores.
   static const bool tma_store_env = env_int("AXONN_TMA_STORE", 1) != 0;
