@@ -129,7 +129,10 @@ typedef struct axonn_fc* axonn_fc_t;
 
 /* Create a layer handle on the current grid; validates divisibility and
  * allocates the handle-owned buffers (gathered W_{j,i} when Gz>1, the dW
- * partial when Gz>1).  Errors: ARG, STATE (no grid), SHAPE, CUDA. */
+ * partial when Gz>1, the symmetric buffers of the fused collectives).  bf16
+ * layers also need k_l and n_l to be multiples of 8 (TMA rows are 16-byte
+ * aligned); m_l is unrestricted.  Errors: ARG, STATE (no grid), SHAPE, CUDA,
+ * NCCL. */
 axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out);
 /* Geometry of this rank for handle `h` (host out). */
 axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);

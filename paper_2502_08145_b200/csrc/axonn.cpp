@@ -592,6 +592,10 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
   if (!S.grid) return fail(AXONN_ERR_STATE, "axonn_grid_init must precede axonn_fc_create");
   axonn_geometry_t geo;
   STATUS_TRY(geometry_of(desc, S.g, S.rank, &geo));
+  if (desc->dtype == AXONN_BF16 && (geo.k_l % 8 || geo.n_l % 8))
+    return fail(AXONN_ERR_SHAPE,
+                "bf16 shards need k_l=%lld and n_l=%lld to be multiples of 8 (16-byte rows for TMA)",
+                (long long)geo.k_l, (long long)geo.n_l);
   auto* h = new axonn_fc();
   h->d = *desc;
   if (h->d.chunks < 1) h->d.chunks = 1;

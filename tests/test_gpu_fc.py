@@ -118,3 +118,20 @@ def test_cuda_graph_capture_and_replay(ax):
         for got, ref in zip((bufs["O"], bufs["dI"], bufs["dW"].reshape(k, n)), fc.fc_layer(X, W, dY)):
             assert np.array_equal(bf16_bits_of(got), synthdata.bf16_bits(synthdata.bf16_round(ref)))
     ax.axonn_fc_destroy(h)
+
+
+def test_bf16_shards_need_16_byte_rows(ax):
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_fc_create(64, 60, 64)
+    assert e.value.status == ax.AXONN_ERR_SHAPE and "multiples of 8" in str(e.value)
+    h = ax.axonn_fc_create(64, 60, 64, False, ax.AXONN_F32)   # fp32 test mode: no TMA
+    ax.axonn_fc_destroy(h)
+
+
+@pytest.mark.parametrize("m", [1, 127, 129, 1000])
+def test_ragged_token_counts(ax, m):
+    """m_l is unrestricted: a single token and counts that are not tile multiples."""
+    torch = require_cuda()
+    (X, W, dY), outs = _layer(ax, m, 136, 264, False, "int", torch.bfloat16)
+    for got, ref in zip(outs, fc.fc_layer(X, W, dY)):
+        assert np.array_equal(bf16_bits_of(got), synthdata.bf16_bits(synthdata.bf16_round(ref)))
