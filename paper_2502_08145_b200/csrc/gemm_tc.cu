@@ -702,8 +702,8 @@ int env_int(const char* name, int dflt) {
 // C[M][N] (bf16, ldc) = op(A) x op(B); see axonn_gemm in include/axonn.h.
 // AXONN_GEMM_VARIANT=single selects the 1-CTA kernel (kept for A/B timing);
 // the default is the CTA-pair kernel: 512x256 tiles for plain launches
-// (AXONN_PAIR_MT=1: 256x256), 256x256 for fused-collective epilogues
-// (AXONN_PAIR_MT_FUSED=2: 512x256).  AXONN_GROUP_M sets the raster band.
+// (AXONN_PAIR_MT=1: 256x256) and for fused-collective epilogues with K >= 8192,
+// 256x256 for shorter fused launches.  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
                         cudaStream_t stream, const EpiTarget* epi_in) {
@@ -721,7 +721,10 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   // launches; 256x256 (MT=1: double-buffered TMEM, so the NVLink-writing
   // epilogue overlaps the next tile's main loop) for fused-collective epilogues.
   static const int mt_plain = env_int("AXONN_PAIR_MT", 2) == 1 ? 1 : 2;
-  static const int mt_fused = env_int("AXONN_PAIR_MT_FUSED", 1) == 2 ? 2 : 1;
+  // fused epilogues: 512x256 when the K loop is long enough to amortise the
+  // serialised (NVLink-writing) epilogue, else 256x256 (AXONN_PAIR_MT_FUSED=1|2 forces)
+  static const int mt_fused_env = env_int("AXONN_PAIR_MT_FUSED", 0);
+  const int mt_fused = mt_fused_env == 1 ? 1 : mt_fused_env == 2 ? 2 : (K >= 8192 ? 2 : 1);
   CUtensorMap ma, mb;
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
   // B box rows along N: 256 for the single-CTA tile, 128 (half of N) per CTA of a pair.
