@@ -639,15 +639,18 @@ cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C,
 
 int env_int(const char* name, int dflt);
 
-// Dynamic tile scheduling: a ring of global counters, one zeroed per launch
-// (AXONN_SCHED=static disables it and returns nullptr).
+// Dynamic tile scheduling: a ring of global counters, one zeroed (in stream
+// order) per launch.  A slot is reused only after kSlots further launches, so
+// launches on different streams never share a live counter unless more than
+// kSlots GEMMs are in flight at once.  AXONN_SCHED=static disables it.
+// Called under the library mutex.
 int* next_tile_counter(cudaStream_t stream) {
   static const bool dyn = [] {
     const char* v = std::getenv("AXONN_SCHED");
     return !(v && std::strcmp(v, "static") == 0);
   }();
   if (!dyn) return nullptr;
-  constexpr int kSlots = 256;
+  constexpr int kSlots = 16384;
   static int* ring = nullptr;
   static int next = 0;
   if (!ring && cudaMalloc(&ring, kSlots * sizeof(int)) != cudaSuccess) return nullptr;
