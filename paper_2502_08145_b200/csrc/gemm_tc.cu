@@ -275,7 +275,8 @@ struct PairCfg {
   static constexpr int STAGE_BYTES = SMEM_A + SMEM_B;
   static constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each owning half the columns
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 64 * 2;  // per warp: 32 rows x 64 bf16
+  // per warp: two 32 x 64 bf16 staging boxes (the TMA store of one overlaps filling the other)
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * 32 * 64 * 2;
   static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
@@ -471,8 +472,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
-    uint8_t* stage = sEpi + ew * (32 * 64 * 2);
-    const uint32_t stage_u32 = ptx::smem_u32(stage);
+    uint8_t* stage_base = sEpi + ew * (2 * 32 * 64 * 2);
+    int nstore = 0;  // TMA stores issued by this warp (alternate staging boxes)
     for (int seq = 0;; ++seq) {
       const int t = consume_tile(seq, false);
       __syncwarp();
@@ -488,13 +489,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
         const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
 #pragma unroll 1
         for (int c = chalf * 2; c < chalf * 2 + 2; ++c) {
+          const bool tma = use_tma_store && epi.mode == kStore;
+          uint8_t* stage = stage_base + (tma ? (nstore & 1) * (32 * 64 * 2) : 0);
+          const uint32_t stage_u32 = ptx::smem_u32(stage);
+          if (tma) {
+            // the store issued two chunks ago read this box: make sure it is done
+            if (lane == 0) ptx::tma_store_wait_read_le1();
+            __syncwarp();
+          }
+          uint32_t v0[32], v1[32];
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
+                                 static_cast<uint32_t>(c * 64);
+          ptx::tmem_ld_32x32b_x32(taddr, v0);
+          ptx::tmem_ld_32x32b_x32(taddr + 32, v1);
+          ptx::tmem_wait_ld();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
-                                   static_cast<uint32_t>(c * 64 + hh * 32);
-            ptx::tmem_ld_32x32b_x32(taddr, v);
-            ptx::tmem_wait_ld();
+            const uint32_t* v = hh ? v1 : v0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const int j = hh * 4 + q;  // 16-B unit of this row segment
@@ -507,16 +518,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                            : "memory");
             }
           }
-          if (use_tma_store && epi.mode == kStore) {
+          if (tma) {
             // the staged chunk is exactly TMA's 128-B-swizzled 32 x 64 box
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
               ptx::tma_store_2d(&tmC, stage, tc.n0 + c * 64, row0);
               ptx::tma_store_commit();
-              ptx::tma_store_wait_read();  // staging buffer reusable
             }
-            __syncwarp();
+            ++nstore;
             continue;
           }
           __syncwarp();
