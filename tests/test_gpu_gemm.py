@@ -47,11 +47,17 @@ def _run(op, A, B, M, N, dtype, pad=0):
     ldc = round_up(N) + pad
     dA = to_dev(A, dtype, lda)
     dB = to_dev(B, dtype, ldb)
-    dC = empty_dev(M, N, dtype, ldc)
+    # output inside a NaN canary: 40 extra rows and the ld padding must stay NaN
+    # (compute-sanitizer is closed on this pool; this is our out-of-bounds check)
+    guard = torch.full((M + 40, max(ldc, 1)), float("nan"), dtype=dtype, device="cuda")
+    dC = guard[:M, :N]
     K = A.shape[0] if op == "TN" else A.shape[1]
     ax.axonn_gemm(OPS[op], ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16,
                   M, N, K, dA, lda, dB, ldb, dC, ldc)
     torch.cuda.synchronize()
+    assert torch.isnan(guard[M:, :].float()).all(), "write below the last row"
+    if ldc > N:
+        assert torch.isnan(guard[:, N:].float()).all(), "write past the last column"
     return dC
 
 
