@@ -768,11 +768,14 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   static const int mt2_min_k = env_int("AXONN_MT2_MIN_K", 0);
   const int pair_mt = epi.mode != kStore ? mt_fused : (K >= mt2_min_k ? mt_plain : 1);
   // TMA-store epilogue for plain launches when C satisfies TMA's alignment
-  // (16-byte base and row pitch); AXONN_TMA_STORE=0 keeps per-thread stores.
+  // (16-byte base and row pitch) AND rows end on a 16-byte boundary: the store
+  // clips the inner dimension only at 16-byte granularity, so with N % 8 != 0
+  // it would write up to 7 elements past column N-1 (caught by the tests' NaN
+  // canary).  AXONN_TMA_STORE=0 keeps per-thread stores.
   static const bool tma_store_env = env_int("AXONN_TMA_STORE", 1) != 0;
   CUtensorMap mc;
   int use_tma_store = 0;
-  if (!single && epi.mode == kStore && tma_store_env && (ldc & 7) == 0 &&
+  if (!single && epi.mode == kStore && tma_store_env && (ldc & 7) == 0 && (N & 7) == 0 &&
       (reinterpret_cast<uintptr_t>(C) & 15) == 0 && make_map(&mc, C, N, M, ldc, 64, 32))
     use_tma_store = 1;
   else
