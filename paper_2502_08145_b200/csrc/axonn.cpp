@@ -307,12 +307,16 @@ struct axonn_fc {
   axonn::SymBuf wstage;        // AG_z over copy engines: symmetric staging copy of Ŵ
   std::vector<void*> wpeer;    // every Z rank's staging address (LSA)
   cudaEvent_t ev_rsdone = nullptr;  // last fused RS_z finished reading its slots
+  cudaEvent_t ev_wdone = nullptr;   // last deferred data-parallel reduction finished
 };
 
 namespace {
 
-axonn_status_t fused_barrier(int axis, cudaStream_t st) {
-  CUDA_TRY(axonn::sym_barrier(&S.sym[axis], st));
+// Barrier index 0: barriers issued on the caller's stream (and, for Z, the Z
+// stream, which is the only stream issuing Z barriers); index 1: the deferred
+// data-parallel reductions on the DATA stream.
+axonn_status_t fused_barrier(int axis, cudaStream_t st, int index) {
+  CUDA_TRY(axonn::sym_barrier(&S.sym[axis], st, index));
   g_launches.fetch_add(1);
   return AXONN_OK;
 }
@@ -367,7 +371,7 @@ bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64
   return true;
 }
 
-axonn_status_t fused_barrier(int axis, cudaStream_t st);
+axonn_status_t fused_barrier(int axis, cudaStream_t st, int index = 0);
 
 axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
   if (f.epi.mode == axonn::kMcRed) {
@@ -378,8 +382,8 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
   return AXONN_OK;  // scatter: the previous use's final barrier already freed the slots
 }
 
-axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st) {
-  STATUS_TRY(fused_barrier(f.axis, st));  // every rank's epilogue writes have landed
+axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
+  STATUS_TRY(fused_barrier(f.axis, st, index));  // every rank's epilogue writes have landed
   if (f.epi.mode == axonn::kScatter) {
     void* local = nullptr;
     if (f.out_peer)  // 2 ranks: own copy + plain stores to the peer instead of multicast
@@ -387,7 +391,7 @@ axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st) {
     CUDA_TRY(axonn::sym_owner_reduce(&f.recv, &f.out, f.epi.slice, f.epi.P, f.epi.me, S.num_sms,
                                      st, local, f.out_peer));
     g_launches.fetch_add(1);
-    STATUS_TRY(fused_barrier(f.axis, st));  // every owner's broadcast has landed
+    STATUS_TRY(fused_barrier(f.axis, st, index));  // every owner's broadcast has landed
   }
   return AXONN_OK;
 }
@@ -613,7 +617,7 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
       return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", 2 * wbytes));
   }
   for (cudaEvent_t* e : {&h->ev_in, &h->ev_ag, &h->ev_ar, &h->ev_dw, &h->ev_rs, &h->ev_grad,
-                         &h->ev_rsdone})
+                         &h->ev_rsdone, &h->ev_wdone})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
   if (desc->dtype == AXONN_BF16) {
@@ -841,7 +845,10 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   };
   // fused outputs: buffers ready on every rank before any rank's epilogue writes
   if (fI) STATUS_TRY(fused_pre(h->fi, st));
-  if (fW) STATUS_TRY(fused_pre(h->fw, st));
+  if (fW) {
+    CUDA_TRY(cudaStreamWaitEvent(st, h->ev_wdone, 0));  // previous deferred reduction done
+    STATUS_TRY(fused_pre(h->fw, st));
+  }
   if (Pb > 1 && !fI) {
     // line 11, then line 12 on the bwd-axis stream overlapped with line 13 (OAR)
     STATUS_TRY(dI_gemm());
@@ -867,14 +874,25 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     STATUS_TRY(dI_gemm());
   }
   if (fW) count_comm(4, S.g[AX_D], S_el, dt);
-  // fused outputs: every rank's reductions have landed after these
+  // fused dI: every rank's reductions have landed after this
   if (fI) STATUS_TRY(fused_post(h->fi, st));
-  if (fW) STATUS_TRY(fused_post(h->fw, st));
   if (fI && dI_local != h->fi.out.ptr)
     CUDA_TRY(cudaMemcpyAsync(dI_local, h->fi.out.ptr, static_cast<size_t>(g.m_l * g.k_l) * es,
                              cudaMemcpyDeviceToDevice, st));
-  if (fW && dW_hat != h->fw.out.ptr)
-    CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fw.out.ptr, S_el * es, cudaMemcpyDeviceToDevice, st));
+  if (fW) {
+    // the data-parallel reduction completes on the DATA stream, like the
+    // paper's ORS: only axonn_grads_sync waits for it, so its barriers (which
+    // absorb rank skew) and owner phase stay off this stream
+    cudaStream_t ds = S.cstream[AX_D];
+    CUDA_TRY(cudaEventRecord(h->ev_rs, st));
+    CUDA_TRY(cudaStreamWaitEvent(ds, h->ev_rs, 0));
+    STATUS_TRY(fused_post(h->fw, ds, 1));
+    if (dW_hat != h->fw.out.ptr)
+      CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fw.out.ptr, S_el * es, cudaMemcpyDeviceToDevice, ds));
+    CUDA_TRY(cudaEventRecord(h->ev_wdone, ds));
+    CUDA_TRY(cudaEventRecord(h->ev_grad, ds));
+    last = h->ev_grad;
+  }
   if (last) {
     bool seen = false;
     for (auto e : S.pending_grads) seen = seen || (e == last);
@@ -900,7 +918,8 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
   if (!S.handles.count(h)) return fail(AXONN_ERR_ARG, "unknown handle");
   S.handles.erase(h);
   cudaDeviceSynchronize();
-  for (cudaEvent_t e : {h->ev_in, h->ev_ag, h->ev_ar, h->ev_dw, h->ev_rs, h->ev_grad, h->ev_rsdone}) {
+  for (cudaEvent_t e : {h->ev_in, h->ev_ag, h->ev_ar, h->ev_dw, h->ev_rs, h->ev_grad, h->ev_rsdone,
+                        h->ev_wdone}) {
     if (!e) continue;
     for (size_t i = 0; i < S.pending_grads.size(); ++i)
       if (S.pending_grads[i] == e) S.pending_grads.erase(S.pending_grads.begin() + i--);

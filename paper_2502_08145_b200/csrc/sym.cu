@@ -98,8 +98,8 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, in
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
-__global__ void k_barrier(ncclDevComm dc) {
-  ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), 0);
+__global__ void k_barrier(ncclDevComm dc, uint32_t index) {
+  ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), index);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 }
 
@@ -117,7 +117,7 @@ bool sym_axis_init(ncclComm_t comm, SymAxis* out, std::string* why) {
   ncclDevCommRequirements reqs;
   std::memset(&reqs, 0, sizeof reqs);
   reqs.lsaMultimem = true;
-  reqs.lsaBarrierCount = 1;
+  reqs.lsaBarrierCount = 2;  // one barrier sequence per issuing stream (see sym_barrier)
   ncclResult_t r = ncclDevCommCreate(comm, &reqs, &im->dev);
   if (r != ncclSuccess) {
     *why = std::string("ncclDevCommCreate: ") + ncclGetErrorString(r);
@@ -214,16 +214,16 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  sym_barrier(a, 0);
+  sym_barrier(a, 0, 0);
   k_probe<<<ctas, 512>>>(static_cast<uint4*>(b->ptr), target, n16, mode);
-  sym_barrier(a, 0);
+  sym_barrier(a, 0, 0);
   cudaEventRecord(e0, 0);
   for (int i = 0; i < iters; ++i) k_probe<<<ctas, 512>>>(static_cast<uint4*>(b->ptr), target, n16, mode);
   cudaEventRecord(e1, 0);
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(ms, e0, e1);
   *ms /= iters;
-  sym_barrier(a, 0);
+  sym_barrier(a, 0, 0);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return cudaDeviceSynchronize();
@@ -246,8 +246,8 @@ cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long sl
   return cudaGetLastError();
 }
 
-cudaError_t sym_barrier(SymAxis* a, cudaStream_t st) {
-  k_barrier<<<1, 32, 0, st>>>(a->impl->dev);
+cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index) {
+  k_barrier<<<1, 32, 0, st>>>(a->impl->dev, static_cast<uint32_t>(index));
   return cudaGetLastError();
 }
 

@@ -39,7 +39,10 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
                              int me, int num_sms, cudaStream_t st, void* out_local = nullptr,
                              void* out_peer = nullptr);
-// One-CTA cross-rank barrier on `st` (system-scope release/acquire).
-cudaError_t sym_barrier(SymAxis* a, cudaStream_t st);
+// One-CTA cross-rank barrier on `st` (system-scope release/acquire).  Each
+// `index` (0 or 1) is its own barrier sequence: every rank must issue the
+// barriers of one index in the same order, and all barriers of one index must
+// be issued on one stream (the epoch state is not safe under concurrency).
+cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0);
 
 }  // namespace axonn
