@@ -46,7 +46,11 @@ typedef enum {
 
 typedef enum {
   AXONN_BF16 = 0,             /* bf16 storage, fp32 accumulate on tcgen05 */
-  AXONN_F32 = 1               /* fp32 storage and SIMT fp32 arithmetic: test mode            */
+  AXONN_F32 = 1,              /* fp32 storage and SIMT fp32 arithmetic: test mode            */
+  AXONN_BF16_GRADF32 = 2      /* bf16 operands, activations and W; the weight gradient dŴ is
+                                 fp32 (the dW product's accumulator is stored unrounded) and
+                                 RS_z / the data-parallel all-reduce sum fp32 (b = 4 in
+                                 Eqs. 2, 5, reading R17)               */
 } axonn_dtype_t;
 
 /* Message of the last failing call on this thread ("" if none). Never NULL. */
@@ -139,7 +143,7 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
 
 /* Handle-owned output buffers of the fused GEMM + all-reduce path (B200
  * NVLS): which = 0 -> O_local, 1 -> dI_local, 2 -> dW_hat.  *ptr is NULL when
- * that output takes the NCCL path (axis size != 2, fp32 mode, a row length
+ * that output takes the NCCL path (fp32 mode, an fp32 dŴ, a row length
  * not a multiple of 8, or AXONN_FUSED=0).  Passing the returned pointer as the
  * output argument of axonn_fc_forward / axonn_fc_backward avoids the final
  * device-to-device copy; its contents are valid until the next call that
@@ -183,7 +187,8 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
  *             PAPER.md:660-669): it completes at axonn_grads_sync
  *   if Gd > 1: dW_hat += all-reduce over DATA (sum, R9),
  *             issued right after this layer's reduce-scatter.
- * dO_local [m_l][n_l], dI_local [m_l][k_l], dW_hat [what_len].  dI_local is
+ * dO_local [m_l][n_l], dI_local [m_l][k_l], dW_hat [what_len] (fp32 when
+ * desc.dtype is AXONN_BF16_GRADF32, else desc.dtype).  dI_local is
  * ready in `stream` order when this call returns; dW_hat only after
  * axonn_grads_sync(stream).  Errors: STATE (no forward since the last
  * backward), ARG, CUDA, NCCL. */
@@ -205,7 +210,10 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h);
 /* Row-major, leading dimensions lda/ldb/ldc in elements (multiples of 8 for */
 /* bf16, 16-byte aligned base pointers).  bf16: tcgen05.mma kind::f16 with   */
 /* fp32 accumulation in TMEM, one RNE rounding to bf16 at the end.  f32: SIMT*/
-/* fp32 FMA (test mode).  M, N, K >= 0 (K == 0 writes zeros).                */
+/* fp32 FMA (test mode).  AXONN_BF16_GRADF32 (op TN only, else ARG): bf16   */
+/* A and B on tcgen05, C fp32 = the unrounded TMEM accumulator (ldc % 4 == 0 */
+/* for the TMA-store epilogue, any ldc otherwise).                           */
+/* M, N, K >= 0 (K == 0 writes zeros).                                       */
 /* ======================================================================== */
 typedef enum { AXONN_OP_NN = 0, AXONN_OP_NT = 1, AXONN_OP_TN = 2 } axonn_op_t;
 
@@ -272,6 +280,16 @@ axonn_status_t axonn_grid_select(const axonn_layer_t* layers, int n_layers, int 
                                  const axonn_bw_entry_t* table, int n_table, double beta_inter,
                                  int bytes_per_elem, int fixed_gd, axonn_grid_score_t* out,
                                  int cap, int* n_out);
+
+/* Mixed precision (reading R17): as axonn_grid_select,
+ * with b = bytes_per_elem in Eqs. 1, 3, 4 (weights and activations) and
+ * b = grad_bytes_per_elem in Eqs. 2 and 5 (the gradient reductions; 4 for
+ * layers created with AXONN_BF16_GRADF32).  axonn_grid_select(b) ==
+ * axonn_grid_select_mp(b, b). */
+axonn_status_t axonn_grid_select_mp(const axonn_layer_t* layers, int n_layers, int G, int g_node,
+                                    const axonn_bw_entry_t* table, int n_table, double beta_inter,
+                                    int bytes_per_elem, int grad_bytes_per_elem, int fixed_gd,
+                                    axonn_grid_score_t* out, int cap, int* n_out);
 
 #ifdef __cplusplus
 }

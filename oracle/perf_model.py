@@ -76,13 +76,16 @@ def effective_bandwidths(cfg, g_node: int, table: dict, beta_inter: float):
     return tuple(betas)
 
 
-def layer_bytes(layer: Layer, cfg, b: int = 2):
+def layer_bytes(layer: Layer, cfg, b: int = 2, b_grad: int | None = None):
     """Per-rank bytes of Eqs. 1-5 for one layer, exact.
 
     Returns dict with keys ag_z, rs_z, ar_y (Eq. 3 form: the forward
     all-reduce), ar_x (Eq. 4 form: the backward dI all-reduce), ar_d, and
-    the axes they physically run on.
+    the axes they physically run on.  b_grad (default b) is the element size
+    of the two gradient reductions, Eqs. 2 and 5 (reading R17: gradients
+    reduced in fp32 while weights and activations move in bf16).
     """
+    bg = b if b_grad is None else b_grad
     gx, gy, gz, gd = cfg
     if layer.transposed:               # PAPER.md:488-489: swap Gx and Gy
         gx, gy = gy, gx
@@ -91,20 +94,20 @@ def layer_bytes(layer: Layer, cfg, b: int = 2):
     F = Fraction
     return {
         "ag_z": F(gz - 1) * F(k * n, gx * gy * gz) * b,
-        "rs_z": F(gz - 1, gz) * F(k * n, gx * gy) * b,
+        "rs_z": F(gz - 1, gz) * F(k * n, gx * gy) * bg,
         "ar_y": 2 * F(gy - 1, gy) * m * F(n, gz * gx) * b,
         "ar_x": 2 * F(gx - 1, gx) * m * F(k, gz * gy) * b,
-        "ar_d": 2 * F(gd - 1, gd) * F(k * n, gx * gy * gz) * b,
+        "ar_d": 2 * F(gd - 1, gd) * F(k * n, gx * gy * gz) * bg,
     }
 
 
-def layer_times(layer: Layer, cfg, betas, b: int = 2):
+def layer_times(layer: Layer, cfg, betas, b: int = 2, b_grad: int | None = None):
     """Eqs. 1-6 for one layer: exact rational seconds per term and t_comm."""
     bx, by, bz, bd = betas
     if layer.transposed:               # swap β of X and Y with G (R10)
         bx, by = by, bx
     by_term = {"ag_z": bz, "rs_z": bz, "ar_y": by, "ar_x": bx, "ar_d": bd}
-    byts = layer_bytes(layer, cfg, b)
+    byts = layer_bytes(layer, cfg, b, b_grad)
     t = {}
     for key, nbytes in byts.items():
         beta = by_term[key]
@@ -122,18 +125,18 @@ def feasible(layer: Layer, cfg) -> bool:
     return ((layer.k // ga) * (layer.n // gb)) % gz == 0
 
 
-def network_times(layers, cfg, betas, b: int = 2):
+def network_times(layers, cfg, betas, b: int = 2, b_grad: int | None = None):
     """Sum of Eq. 6 over all layers."""
     tot = {key: Fraction(0) for key in ("ag_z", "rs_z", "ar_y", "ar_x", "ar_d", "comm")}
     for L in layers:
-        t = layer_times(L, cfg, betas, b)
+        t = layer_times(L, cfg, betas, b, b_grad)
         for key in tot:
             tot[key] += t[key]
     return tot
 
 
 def rank_configs(layers, G: int, g_node: int, table: dict, beta_inter: float,
-                 b: int = 2, fixed_gd: int = 0):
+                 b: int = 2, fixed_gd: int = 0, b_grad: int | None = None):
     """Ordered list of (cfg, times) — the model's ranking.
 
     Enumerates every (Gx, Gy, Gz, Gd) with product G, drops the ones that do
@@ -146,7 +149,7 @@ def rank_configs(layers, G: int, g_node: int, table: dict, beta_inter: float,
         if not all(feasible(L, cfg) for L in layers):
             continue
         betas = effective_bandwidths(cfg, g_node, table, beta_inter)
-        out.append((cfg, network_times(layers, cfg, betas, b)))
+        out.append((cfg, network_times(layers, cfg, betas, b, b_grad)))
     if not out:
         raise ValueError("infeasible: no configuration divides every layer")
     out.sort(key=lambda e: (e[1]["comm"], e[0]))

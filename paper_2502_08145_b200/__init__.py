@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
 # ---------------------------------------------------------------- constants
 AXONN_OK, AXONN_ERR_ARG, AXONN_ERR_CONFIG, AXONN_ERR_SHAPE, AXONN_ERR_STATE = 0, 1, 2, 3, 4
 AXONN_ERR_INFEASIBLE, AXONN_ERR_CUDA, AXONN_ERR_NCCL, AXONN_ERR_UNSUPPORTED = 5, 6, 7, 8
-AXONN_BF16, AXONN_F32 = 0, 1
+AXONN_BF16, AXONN_F32, AXONN_BF16_GRADF32 = 0, 1, 2
 AXONN_OP_NN, AXONN_OP_NT, AXONN_OP_TN = 0, 1, 2
 AXIS = {"x": 0, "y": 1, "z": 2, "d": 3}
 _STATUS_NAMES = {0: "OK", 1: "ARG", 2: "CONFIG", 3: "SHAPE", 4: "STATE", 5: "INFEASIBLE",
@@ -100,6 +100,9 @@ _PROTOS = {
     "axonn_comm_bytes": (_S, [POINTER(c_int64), c_int]),
     "axonn_grid_select": (_S, [POINTER(LayerT), c_int, c_int, c_int, POINTER(BwEntry), c_int,
                                c_double, c_int, c_int, POINTER(GridScore), c_int, POINTER(c_int)]),
+    "axonn_grid_select_mp": (_S, [POINTER(LayerT), c_int, c_int, c_int, POINTER(BwEntry), c_int,
+                                  c_double, c_int, c_int, c_int, POINTER(GridScore), c_int,
+                                  POINTER(c_int)]),
 }
 for _name, (_res, _args) in _PROTOS.items():
     _f = getattr(_lib, _name)
@@ -277,10 +280,12 @@ def axonn_comm_bytes(reset: bool = False) -> dict:
 
 
 def axonn_grid_select(layers, G, g_node, table, beta_inter, bytes_per_elem=2, fixed_gd=0,
-                      cap=None):
+                      cap=None, grad_bytes_per_elem=None):
     """layers: iterable of (m, k, n, transposed); table: {(G0, G1): bytes/s}.
 
-    Returns the ranked list of dicts (gx, gy, gz, gd, t_ag_z, ..., t_comm)."""
+    Returns the ranked list of dicts (gx, gy, gz, gd, t_ag_z, ..., t_comm).
+    grad_bytes_per_elem (default: bytes_per_elem) is b of Eqs. 2 and 5
+    (axonn_grid_select_mp)."""
     layers = list(layers)
     L = (LayerT * max(1, len(layers)))(*[LayerT(m, k, n, int(bool(t))) for m, k, n, t in layers])
     items = sorted(table.items())
@@ -288,9 +293,21 @@ def axonn_grid_select(layers, G, g_node, table, beta_inter, bytes_per_elem=2, fi
     cap = 4096 if cap is None else cap
     out = (GridScore * max(1, cap))()
     n = c_int()
-    _check(_lib.axonn_grid_select(L, len(layers), G, g_node, T, len(items), beta_inter,
-                                  bytes_per_elem, fixed_gd, out, cap, byref(n)))
+    if grad_bytes_per_elem is None:
+        _check(_lib.axonn_grid_select(L, len(layers), G, g_node, T, len(items), beta_inter,
+                                      bytes_per_elem, fixed_gd, out, cap, byref(n)))
+    else:
+        _check(_lib.axonn_grid_select_mp(L, len(layers), G, g_node, T, len(items), beta_inter,
+                                         bytes_per_elem, grad_bytes_per_elem, fixed_gd, out, cap,
+                                         byref(n)))
     return [{f: getattr(out[i], f) for f, _ in GridScore._fields_} for i in range(min(cap, n.value))]
+
+
+def axonn_grid_select_mp(layers, G, g_node, table, beta_inter, bytes_per_elem=2,
+                         grad_bytes_per_elem=4, fixed_gd=0, cap=None):
+    """axonn_grid_select with b = grad_bytes_per_elem in Eqs. 2 and 5."""
+    return axonn_grid_select(layers, G, g_node, table, beta_inter, bytes_per_elem, fixed_gd, cap,
+                             grad_bytes_per_elem=grad_bytes_per_elem)
 
 
 # ---------------------------------------------------------------- helpers
@@ -313,7 +330,10 @@ def bootstrap_from_torch_distributed(device: int | None = None) -> None:
 def gemm(op, A, B, C, stream=None) -> None:
     """axonn_gemm on torch tensors (row-major, contiguous rows)."""
     import torch
-    dtype = AXONN_F32 if C.dtype == torch.float32 else AXONN_BF16
+    if C.dtype == torch.float32:
+        dtype = AXONN_BF16_GRADF32 if A.dtype == torch.bfloat16 else AXONN_F32
+    else:
+        dtype = AXONN_BF16
     M, N = C.shape
     K = A.shape[0] if op == AXONN_OP_TN else A.shape[1]
     axonn_gemm(op, dtype, M, N, K, A, A.stride(0), B, B.stride(0), C, C.stride(0), stream)

@@ -109,10 +109,16 @@ int env_int(const char* name, int dflt) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+// Activations and weights (O, dI, W, AG_z, AR_x/y): the dtype's storage.
 inline size_t elem_size(int dtype) { return dtype == AXONN_F32 ? 4 : 2; }
 inline ncclDataType_t nccl_type(int dtype) {
   return dtype == AXONN_F32 ? ncclFloat32 : ncclBfloat16;
 }
+// The weight gradient (dWpart, dŴ, RS_z, data-parallel AR): fp32 for
+// AXONN_BF16_GRADF32 (reading R17).
+inline int act_dtype(int dtype) { return dtype == AXONN_BF16_GRADF32 ? AXONN_BF16 : dtype; }
+inline int grad_dtype(int dtype) { return dtype == AXONN_BF16 ? AXONN_BF16 : AXONN_F32; }
+inline bool valid_dtype(int d) { return d == AXONN_BF16 || d == AXONN_F32 || d == AXONN_BF16_GRADF32; }
 
 // Fail loudly unless the current device is an sm_100 part (the kernels are
 // compiled for sm_100a only; there is no other path).
@@ -163,7 +169,7 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
                         cudaStream_t st, const axonn::EpiTarget* epi = nullptr) {
   STATUS_TRY(ensure_device());
   if (M == 0 || N == 0) return AXONN_OK;
-  const size_t es = elem_size(dtype);
+  const size_t es = dtype == AXONN_BF16_GRADF32 ? 4 : elem_size(dtype);  // of C
   if (K == 0) {
     // a zero partial: nothing to add into a fused (pre-zeroed) reduction buffer
     if (epi && epi->mode == axonn::kScatter)
@@ -194,8 +200,9 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
     CUDA_TRY(record(e0));
   }
   axonn::GemmStatus gs;
-  if (dtype == AXONN_BF16)
-    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st, epi);
+  if (dtype == AXONN_BF16 || dtype == AXONN_BF16_GRADF32)
+    gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st, epi,
+                             dtype == AXONN_BF16_GRADF32);
   else
     gs = axonn::gemm_f32_simt(op, M, N, K, static_cast<const float*>(A), lda,
                               static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc, st);
@@ -208,7 +215,9 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
     case axonn::GemmStatus::kTensorMap:
       return fail(AXONN_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
     case axonn::GemmStatus::kBadOp:
-      return fail(AXONN_ERR_ARG, "gemm: op must be 0 (NN), 1 (NT) or 2 (TN)");
+      return fail(AXONN_ERR_ARG, dtype == AXONN_BF16_GRADF32
+                                     ? "gemm: fp32 output is implemented for op 2 (TN) only"
+                                     : "gemm: op must be 0 (NN), 1 (NT) or 2 (TN)");
     default: {
       cudaError_t e = cudaGetLastError();
       return fail(AXONN_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(e));
@@ -237,8 +246,8 @@ axonn_status_t geometry_of(const axonn_fc_desc_t* d, const int g[4], int rank,
                            axonn_geometry_t* out) {
   if (!d || !out) return fail(AXONN_ERR_ARG, "NULL argument");
   if (d->m < 0 || d->k < 0 || d->n < 0) return fail(AXONN_ERR_ARG, "negative dimension");
-  if (d->dtype != AXONN_BF16 && d->dtype != AXONN_F32)
-    return fail(AXONN_ERR_ARG, "dtype must be AXONN_BF16 or AXONN_F32");
+  if (!valid_dtype(d->dtype))
+    return fail(AXONN_ERR_ARG, "dtype must be AXONN_BF16, AXONN_F32 or AXONN_BF16_GRADF32");
   const int G = g[0] * g[1] * g[2] * g[3];
   if (rank < 0 || rank >= G) return fail(AXONN_ERR_ARG, "rank %d outside grid of %d", rank, G);
   const bool t = d->transposed != 0;
@@ -596,7 +605,7 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
   if (!S.grid) return fail(AXONN_ERR_STATE, "axonn_grid_init must precede axonn_fc_create");
   axonn_geometry_t geo;
   STATUS_TRY(geometry_of(desc, S.g, S.rank, &geo));
-  if (desc->dtype == AXONN_BF16 && (geo.k_l % 8 || geo.n_l % 8))
+  if (desc->dtype != AXONN_F32 && (geo.k_l % 8 || geo.n_l % 8))
     return fail(AXONN_ERR_SHAPE,
                 "bf16 shards need k_l=%lld and n_l=%lld to be multiples of 8 (16-byte rows for TMA)",
                 (long long)geo.k_l, (long long)geo.n_l);
@@ -607,24 +616,27 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
   h->ax_fwd = desc->transposed ? AX_X : AX_Y;
   h->ax_bwd = desc->transposed ? AX_Y : AX_X;
   const size_t wbytes = static_cast<size_t>(geo.k_l) * geo.n_l * elem_size(desc->dtype);
+  const size_t gbytes = static_cast<size_t>(geo.k_l) * geo.n_l * elem_size(grad_dtype(desc->dtype));
   auto cleanup = [&](axonn_status_t s) {
     axonn_fc_destroy(h);
     return s;
   };
   S.handles.insert(h);
   if (S.g[AX_Z] > 1 && wbytes) {
-    if (cudaMalloc(&h->wbuf, wbytes) != cudaSuccess || cudaMalloc(&h->dwpart, wbytes) != cudaSuccess)
-      return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", 2 * wbytes));
+    if (cudaMalloc(&h->wbuf, wbytes) != cudaSuccess || cudaMalloc(&h->dwpart, gbytes) != cudaSuccess)
+      return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", wbytes + gbytes));
   }
   for (cudaEvent_t* e : {&h->ev_in, &h->ev_ag, &h->ev_ar, &h->ev_dw, &h->ev_rs, &h->ev_grad,
                          &h->ev_rsdone, &h->ev_wdone})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
-  if (desc->dtype == AXONN_BF16) {
+  if (desc->dtype != AXONN_F32) {
+    // the fused epilogues reduce bf16; an fp32 dŴ takes NCCL
     std::string why;
     if (!fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, &why) ||
         !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, &why) ||
-        (S.g[AX_Z] == 1 && !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why)))
+        (desc->dtype == AXONN_BF16 && S.g[AX_Z] == 1 &&
+         !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why)))
       return cleanup(fail(AXONN_ERR_NCCL, "fused all-reduce buffers: %s", why.c_str()));
   }
   if (desc->dtype == AXONN_BF16 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
@@ -726,7 +738,7 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
     // over NVLink (fused_setup); barriers order the buffer reuse.
     const size_t bytes = static_cast<size_t>(g.m_l * g.n_l) * es;
     STATUS_TRY(fused_pre(h->fo, st));
-    STATUS_TRY(run_gemm(AXONN_OP_NN, h->d.dtype, g.m_l, g.n_l, g.k_l, I_local, g.k_l, W, g.n_l,
+    STATUS_TRY(run_gemm(AXONN_OP_NN, act_dtype(h->d.dtype), g.m_l, g.n_l, g.k_l, I_local, g.k_l, W, g.n_l,
                         h->fo.out.ptr, g.n_l, st, &h->fo.epi));
     STATUS_TRY(fused_post(h->fo, st));
     count_comm(2, P, static_cast<size_t>(g.m_l * g.n_l), h->d.dtype);
@@ -748,7 +760,7 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
     const int64_t rows = std::min<int64_t>(rows_per, g.m_l - r0);
     const char* Ic = static_cast<const char*>(I_local) + r0 * g.k_l * es;
     char* Oc = static_cast<char*>(O_local) + r0 * g.n_l * es;
-    STATUS_TRY(run_gemm(AXONN_OP_NN, h->d.dtype, rows, g.n_l, g.k_l, Ic, g.k_l, W, g.n_l, Oc,
+    STATUS_TRY(run_gemm(AXONN_OP_NN, act_dtype(h->d.dtype), rows, g.n_l, g.k_l, Ic, g.k_l, W, g.n_l, Oc,
                         g.n_l, st));
     if (P > 1 && rows > 0) {
       cudaEvent_t ev = h->ev_chunk[std::min<size_t>(c, h->ev_chunk.size() - 1)];
@@ -784,6 +796,9 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   cudaStream_t st = as_stream(stream);
   const int dt = h->d.dtype;
   const ncclDataType_t nt = nccl_type(dt);
+  const int gdt = grad_dtype(dt);             // dWpart / dŴ and their reductions
+  const ncclDataType_t gnt = nccl_type(gdt);
+  const int adt = act_dtype(dt);              // the dI product
   const int Pb = S.g[h->ax_bwd];
   cudaStream_t bs = S.cstream[h->ax_bwd];
   const bool rs = S.g[AX_Z] > 1;
@@ -796,7 +811,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   cudaEvent_t last = nullptr;
   // line 11: dI^ = dO x W^T  (M = m_l, N = k_l, K = n_l)
   auto dI_gemm = [&]() -> axonn_status_t {
-    return run_gemm(AXONN_OP_NT, dt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
+    return run_gemm(AXONN_OP_NT, adt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
                     fI ? h->fi.out.ptr : dI_local, g.k_l, st, fI ? &h->fi.epi : nullptr);
   };
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
@@ -826,18 +841,18 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     } else if (rs) {
       CUDA_TRY(cudaEventRecord(h->ev_rs, st));
       CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
-      NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_Z],
+      NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, gnt, ncclSum, S.axis_comm[AX_Z],
                                  S.cstream[AX_Z]));
-      count_comm(1, S.g[AX_Z], S_el, dt);
+      count_comm(1, S.g[AX_Z], S_el, gdt);
       CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_Z]));
       last = h->ev_grad;
     }
     if (S.g[AX_D] > 1) {
       CUDA_TRY(cudaEventRecord(h->ev_rs, rs ? S.cstream[AX_Z] : st));
       CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_D], h->ev_rs, 0));
-      NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, nt, ncclSum, S.axis_comm[AX_D],
+      NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, gnt, ncclSum, S.axis_comm[AX_D],
                              S.cstream[AX_D]));
-      count_comm(4, S.g[AX_D], S_el, dt);
+      count_comm(4, S.g[AX_D], S_el, gdt);
       CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_D]));
       last = h->ev_grad;
     }
@@ -943,7 +958,7 @@ axonn_status_t axonn_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, co
                           void* stream) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (op < 0 || op > 2) return fail(AXONN_ERR_ARG, "op must be 0 (NN), 1 (NT) or 2 (TN)");
-  if (dtype != AXONN_BF16 && dtype != AXONN_F32) return fail(AXONN_ERR_ARG, "bad dtype");
+  if (!valid_dtype(dtype)) return fail(AXONN_ERR_ARG, "bad dtype");
   if (M < 0 || N < 0 || K < 0) return fail(AXONN_ERR_ARG, "negative dimension");
   if (M && N && (!C || (K && (!A || !B)))) return fail(AXONN_ERR_ARG, "NULL matrix");
   const int64_t a_cols = (op == AXONN_OP_TN) ? M : K;
@@ -1002,8 +1017,17 @@ axonn_status_t axonn_grid_select(const axonn_layer_t* layers, int n_layers, int 
                                  const axonn_bw_entry_t* table, int n_table, double beta_inter,
                                  int bytes_per_elem, int fixed_gd, axonn_grid_score_t* out,
                                  int cap, int* n_out) {
+  return axonn_grid_select_mp(layers, n_layers, G, g_node, table, n_table, beta_inter,
+                              bytes_per_elem, bytes_per_elem, fixed_gd, out, cap, n_out);
+}
+
+axonn_status_t axonn_grid_select_mp(const axonn_layer_t* layers, int n_layers, int G, int g_node,
+                                    const axonn_bw_entry_t* table, int n_table, double beta_inter,
+                                    int bytes_per_elem, int grad_bytes_per_elem, int fixed_gd,
+                                    axonn_grid_score_t* out, int cap, int* n_out) {
   if ((!layers && n_layers) || n_layers < 0 || G < 1 || g_node < 1 || (!table && n_table) ||
-      n_table < 0 || !(beta_inter > 0) || bytes_per_elem < 1 || cap < 0 || (!out && cap) || !n_out)
+      n_table < 0 || !(beta_inter > 0) || bytes_per_elem < 1 || grad_bytes_per_elem < 1 ||
+      cap < 0 || (!out && cap) || !n_out)
     return fail(AXONN_ERR_ARG, "bad argument to axonn_grid_select");
   std::vector<axonn::Layer> ls;
   for (int i = 0; i < n_layers; ++i) {
@@ -1018,8 +1042,8 @@ axonn_status_t axonn_grid_select(const axonn_layer_t* layers, int n_layers, int 
   }
   std::vector<axonn::Scored> ranked;
   std::string err;
-  const int n = axonn::rank_configs(ls, G, g_node, tb, beta_inter, bytes_per_elem, fixed_gd,
-                                    &ranked, &err);
+  const int n = axonn::rank_configs(ls, G, g_node, tb, beta_inter, bytes_per_elem,
+                                    grad_bytes_per_elem, fixed_gd, &ranked, &err);
   if (n < 0) return fail(AXONN_ERR_CONFIG, "configuration error: %s", err.c_str());
   *n_out = n;
   if (n == 0) return fail(AXONN_ERR_INFEASIBLE, "infeasible: no configuration of %d GPUs divides every layer", G);

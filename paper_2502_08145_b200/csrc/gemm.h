@@ -27,9 +27,10 @@ enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2 };
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 
 // bf16 x bf16 -> bf16 (fp32 accumulate) on tcgen05; op 0 = NN, 1 = NT, 2 = TN.
+// out_f32: C is fp32 (op 2 only: the dW product of fp32 gradient reduction).
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream, const EpiTarget* epi = nullptr);
+                        cudaStream_t stream, const EpiTarget* epi = nullptr, bool out_f32 = false);
 
 // fp32 SIMT FMA (test mode, no TF32): same op codes.
 GemmStatus gemm_f32_simt(int op, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

@@ -280,12 +280,14 @@ struct PairCfg {
   static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
-template <int A_MN, int B_MN, int MT>
+// OUTF = 1: fp32 output (the dW GEMM when gradients are reduced in fp32,
+// SURVEY.md §8(f) f-4): the accumulator is stored without rounding.
+template <int A_MN, int B_MN, int MT, int OUTF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmC, int use_tma_store,
-                           __nv_bfloat16* __restrict__ C, int64_t ldc, int M, int N, int K,
+                           void* __restrict__ Cv, int64_t ldc, int M, int N, int K,
                            int group_m, const __grid_constant__ EpiTarget epi,
                            int* __restrict__ tile_counter) {
   using Cfg = PairCfg<MT>;
@@ -469,9 +471,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
     const int ew = warp - 4;          // epilogue warp 0..7
     const int e = ew & 3;             // TMEM lane quarter (warp % 4)
     const int chalf = ew >> 2;        // which 128 columns of the tile this warp stores
+    constexpr int ELEM = OUTF ? 4 : 2;        // bytes per output element
+    constexpr int CCOLS = 128 / ELEM;         // columns per staged chunk (128-B rows)
+    constexpr int UCOLS = 16 / ELEM;          // columns per 16-B unit
+    constexpr int NCH = 128 / CCOLS;          // chunks per warp (its 128 columns)
+    char* const Cb = static_cast<char*>(Cv);
+    __nv_bfloat16* const C = static_cast<__nv_bfloat16*>(Cv);
     int acc = 0;
     uint32_t acc_phase = 0;
-    const bool vec_ok = ((ldc & 7) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+    const bool vec_ok =
+        ((ldc * ELEM) % 16 == 0) && ((reinterpret_cast<uintptr_t>(Cv) & 15) == 0);
     uint8_t* stage_base = sEpi + ew * (2 * 32 * 64 * 2);
     int nstore = 0;  // TMA stores issued by this warp (alternate staging boxes)
     for (int seq = 0;; ++seq) {
@@ -488,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
         const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
         const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
 #pragma unroll 1
-        for (int c = chalf * 2; c < chalf * 2 + 2; ++c) {
+        for (int c = chalf * NCH; c < chalf * NCH + NCH; ++c) {
           const bool tma = use_tma_store && epi.mode == kStore;
           uint8_t* stage = stage_base + (tma ? (nstore & 1) * (32 * 64 * 2) : 0);
           const uint32_t stage_u32 = ptx::smem_u32(stage);
@@ -497,33 +506,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
             if (lane == 0) ptx::tma_store_wait_read_le1();
             __syncwarp();
           }
-          uint32_t v0[32], v1[32];
           const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
-                                 static_cast<uint32_t>(c * 64);
-          ptx::tmem_ld_32x32b_x32(taddr, v0);
-          ptx::tmem_ld_32x32b_x32(taddr + 32, v1);
-          ptx::tmem_wait_ld();
+                                 static_cast<uint32_t>(c * CCOLS);
+          if (OUTF) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(taddr, v);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t* v = hh ? v1 : v0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int j = hh * 4 + q;  // 16-B unit of this row segment
+            for (int j = 0; j < 8; ++j) {  // 16-B unit = 4 fp32 columns
               const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                           "r"(ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1])),
-                           "r"(ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
-                           "r"(ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5])),
-                           "r"(ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v[4 * j]),
+                           "r"(v[4 * j + 1]), "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
                            : "memory");
+            }
+          } else {
+            uint32_t v0[32], v1[32];
+            ptx::tmem_ld_32x32b_x32(taddr, v0);
+            ptx::tmem_ld_32x32b_x32(taddr + 32, v1);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const uint32_t* v = hh ? v1 : v0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int j = hh * 4 + q;  // 16-B unit = 8 bf16 columns
+                const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                             "r"(ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1])),
+                             "r"(ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
+                             "r"(ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5])),
+                             "r"(ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
+                             : "memory");
+              }
             }
           }
           if (tma) {
-            // the staged chunk is exactly TMA's 128-B-swizzled 32 x 64 box
+            // the staged chunk is exactly TMA's 128-B-swizzled 32-row box
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              ptx::tma_store_2d(&tmC, stage, tc.n0 + c * 64, row0);
+              ptx::tma_store_2d(&tmC, stage, tc.n0 + c * CCOLS, row0);
               ptx::tma_store_commit();
             }
             ++nstore;
@@ -531,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           }
           __syncwarp();
           const int u = lane & 7;
-          const int gcol = tc.n0 + c * 64 + u * 8;
+          const int gcol = tc.n0 + c * CCOLS + u * UCOLS;
 #pragma unroll 2
           for (int it = 0; it < 8; ++it) {
             const int r = it * 4 + (lane >> 3);
@@ -554,8 +576,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                 const long long off =
                     static_cast<long long>(epi.me) * epi.slice + (f - o * epi.slice);
                 *reinterpret_cast<uint4*>(epi.peer[o] + static_cast<uint64_t>(off) * 2) = w;
-              } else if (vec_ok && gcol + 8 <= N) {
-                *reinterpret_cast<uint4*>(C + static_cast<int64_t>(grow) * ldc + gcol) = w;
+              } else if (vec_ok && gcol + UCOLS <= N) {
+                *reinterpret_cast<uint4*>(Cb + (static_cast<int64_t>(grow) * ldc + gcol) * ELEM) = w;
+              } else if (OUTF) {
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+                float* dst = reinterpret_cast<float*>(Cb) + static_cast<int64_t>(grow) * ldc + gcol;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  if (gcol + q < N) dst[q] = __uint_as_float(ws[q]);
               } else {
                 const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
                 __nv_bfloat16* dst = C + static_cast<int64_t>(grow) * ldc + gcol;
@@ -608,11 +636,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // row, `outer` rows, row stride `ld` elements; box box_inner x box_outer with
 // 128-byte swizzle; out-of-bounds elements read as zero.
 bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_inner, uint32_t box_outer) {
+              uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   static const int promo = [] {
@@ -623,7 +651,8 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
       promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
       : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
       : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, p,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -670,12 +699,12 @@ int* next_tile_counter(cudaStream_t stream) {
   return c;
 }
 
-template <int A_MN, int B_MN, int MT>
+template <int A_MN, int B_MN, int MT, int OUTF = 0>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                         int use_tma_store, void* C, int64_t ldc, int M, int N, int K, int num_sms,
                         int group_m, const EpiTarget& epi, cudaStream_t stream) {
   using Cfg = PairCfg<MT>;
-  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT>;
+  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT, OUTF>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -688,8 +717,7 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
   int* counter = next_tile_counter(stream);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, mc, use_tma_store,
-                                                       static_cast<__nv_bfloat16*>(C), ldc, M, N, K,
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
                                                        group_m, epi, counter);
   return cudaGetLastError();
 }
@@ -719,15 +747,16 @@ int env_int(const char* name, int dflt) {
 // 256x256 for shorter fused launches.  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream, const EpiTarget* epi_in) {
+                        cudaStream_t stream, const EpiTarget* epi_in, bool out_f32) {
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return GemmStatus::kBadShape;
   if ((lda & 7) || (ldb & 7) || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
     return GemmStatus::kBadAlignment;
-  static const bool single = [] {
+  static const bool single_env = [] {
     const char* v = std::getenv("AXONN_GEMM_VARIANT");
     return v && std::strcmp(v, "single") == 0;
   }();
+  const bool single = single_env && !out_f32;  // the 1-CTA kernel has no fp32 epilogue
   // raster band: 4096 rows of tiles (AXONN_GROUP_M overrides, in tiles; < 0 = bands of N tiles)
   static const int group_m_env = env_int("AXONN_GROUP_M", 0);
   // 512x256 tiles (MT=2: less L2/DRAM traffic per flop) for plain-store
@@ -759,7 +788,9 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (!ok) return GemmStatus::kTensorMap;
   cudaError_t e;
   const EpiTarget epi = epi_in ? *epi_in : EpiTarget();
-  if (epi.mode != kStore && (single || (N & 7) || (ldc & 7))) return GemmStatus::kBadAlignment;
+  if (epi.mode != kStore && (single || (N & 7) || (ldc & 7) || out_f32))
+    return GemmStatus::kBadAlignment;
+  if (out_f32 && op != 2) return GemmStatus::kBadOp;  // fp32 output: the dW (TN) product only
   if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   // MT=2's single accumulator serialises the epilogue with the next tile; on
@@ -775,13 +806,20 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   static const bool tma_store_env = env_int("AXONN_TMA_STORE", 1) != 0;
   CUtensorMap mc;
   int use_tma_store = 0;
-  if (!single && epi.mode == kStore && tma_store_env && (ldc & 7) == 0 && (N & 7) == 0 &&
-      (reinterpret_cast<uintptr_t>(C) & 15) == 0 && make_map(&mc, C, N, M, ldc, 64, 32))
+  const int cols16 = out_f32 ? 4 : 8;  // elements per 16 bytes of C
+  if (!single && epi.mode == kStore && tma_store_env && (ldc % cols16) == 0 && (N % cols16) == 0 &&
+      (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+      make_map(&mc, C, N, M, ldc, out_f32 ? 32 : 64, 32, out_f32))
     use_tma_store = 1;
   else
     std::memset(&mc, 0, sizeof mc);
   const int group_m = group_m_env != 0 ? group_m_env : (single ? 32 : 16 / pair_mt);
-  if (single) {
+  if (out_f32) {
+    e = pair_mt == 2 ? launch_pair<1, 1, 2, 1>(ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms,
+                                               group_m, epi, stream)
+                     : launch_pair<1, 1, 1, 1>(ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms,
+                                               group_m, epi, stream);
+  } else if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
                   : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);

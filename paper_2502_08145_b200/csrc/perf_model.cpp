@@ -72,7 +72,7 @@ bool effective_bandwidths(const Config& c, int g_node, const std::vector<BwEntry
   return true;
 }
 
-Times layer_times(const Layer& L, const Config& c, const double beta[4], int b) {
+Times layer_times(const Layer& L, const Config& c, const double beta[4], int b, int bg) {
   double gx = c.gx, gy = c.gy, bx = beta[0], by = beta[1];
   if (L.transposed) {  // swap G and beta of X and Y (R10)
     std::swap(gx, gy);
@@ -84,17 +84,17 @@ Times layer_times(const Layer& L, const Config& c, const double beta[4], int b) 
   auto t = [](double bytes, double beta) { return bytes == 0.0 ? 0.0 : bytes / beta; };
   Times r;
   r.ag_z = t((gz - 1) * (k * n / (gx * gy * gz)) * b, bz);                 // Eq. 1
-  r.rs_z = t(((gz - 1) / gz) * (k * n / (gx * gy)) * b, bz);               // Eq. 2
+  r.rs_z = t(((gz - 1) / gz) * (k * n / (gx * gy)) * bg, bz);              // Eq. 2
   r.ar_y = t(2.0 * ((gy - 1) / gy) * (m * n / (gz * gx)) * b, by);         // Eq. 3
   r.ar_x = t(2.0 * ((gx - 1) / gx) * (m * k / (gz * gy)) * b, bx);         // Eq. 4
-  r.ar_d = t(2.0 * ((gd - 1) / gd) * (k * n / (gx * gy * gz)) * b, bd);    // Eq. 5
+  r.ar_d = t(2.0 * ((gd - 1) / gd) * (k * n / (gx * gy * gz)) * bg, bd);   // Eq. 5
   r.comm = r.ag_z + r.rs_z + r.ar_y + r.ar_x + r.ar_d;                     // Eq. 6
   return r;
 }
 
 int rank_configs(const std::vector<Layer>& layers, int G, int g_node,
-                 const std::vector<BwEntry>& table, double beta_inter, int b, int fixed_gd,
-                 std::vector<Scored>* out, std::string* err) {
+                 const std::vector<BwEntry>& table, double beta_inter, int b, int bg,
+                 int fixed_gd, std::vector<Scored>* out, std::string* err) {
   out->clear();
   for (const Config& c : enumerate_configs(G, fixed_gd)) {
     bool ok = true;
@@ -104,7 +104,7 @@ int rank_configs(const std::vector<Layer>& layers, int G, int g_node,
     if (!effective_bandwidths(c, g_node, table, beta_inter, beta, err)) return -1;
     Scored s{c, {}};
     for (const Layer& L : layers) {
-      const Times t = layer_times(L, c, beta, b);
+      const Times t = layer_times(L, c, beta, b, bg);
       s.t.ag_z += t.ag_z;
       s.t.rs_z += t.rs_z;
       s.t.ar_y += t.ar_y;

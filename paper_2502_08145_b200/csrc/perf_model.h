@@ -30,10 +30,13 @@ std::vector<Config> enumerate_configs(int G, int fixed_gd);
 bool feasible(const Layer& L, const Config& c);
 bool effective_bandwidths(const Config& c, int g_node, const std::vector<BwEntry>& table,
                           double beta_inter, double beta[4], std::string* err);
-Times layer_times(const Layer& L, const Config& c, const double beta[4], int bytes_per_elem);
+// b: bytes per element of the activation/weight collectives (Eqs. 1, 3, 4);
+// b_grad: of the gradient reductions (Eqs. 2, 5) — equal unless gradients are
+// reduced in fp32.
+Times layer_times(const Layer& L, const Config& c, const double beta[4], int b, int b_grad);
 // Returns the number of feasible configurations, or -1 with *err set.
 int rank_configs(const std::vector<Layer>& layers, int G, int g_node,
-                 const std::vector<BwEntry>& table, double beta_inter, int bytes_per_elem,
+                 const std::vector<BwEntry>& table, double beta_inter, int b, int b_grad,
                  int fixed_gd, std::vector<Scored>* out, std::string* err);
 
 }  // namespace axonn

@@ -9,7 +9,10 @@ the global O, dI, dW and compares them with the unsharded oracle (oracle.fc):
     fp32 sums of integers are exact) — covers every collective and offset;
   * bf16, uniform inputs: normwise error <= 2e-2;
   * members of every all-reduce group hold bit-identical copies;
-  * the bytes the library hands to NCCL equal Eqs. 1-5 exactly.
+  * the bytes the library hands to NCCL equal Eqs. 1-5 exactly;
+  * AXONN_BF16_GRADF32 (reading R17), integer inputs: dŴ (fp32 GEMM output,
+    fp32 RS_z / data-parallel sums) bit-exact, bytes = Eqs. 1-5 with b = 4 in
+    Eqs. 2 and 5.
 Prints MP_OK on success; any failure raises (non-zero exit).
 """
 import os
@@ -38,9 +41,13 @@ def host(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_copy=False):
+def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_copy=False,
+             grad_f32=False):
     X, W, dY = synthdata.layer_tensors(m, k, n, 7, kind=kind)
     dt = ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16
+    if grad_f32:
+        dt = ax.AXONN_BF16_GRADF32
+    gdtype = torch.float32 if grad_f32 else dtype
     h = ax.axonn_fc_create(m, k, n, transposed, dt, chunks)
     g = ax.axonn_fc_geometry(h)
     I = dev(X[g.row0:g.row0 + g.m_l, g.in_col0:g.in_col0 + g.k_l], dtype)
@@ -50,7 +57,7 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_co
     dO = dev(dY[g.row0:g.row0 + g.m_l, g.out_col0:g.out_col0 + g.n_l], dtype)
     O = torch.full((g.m_l, g.n_l), float("nan"), dtype=dtype, device="cuda")
     dI = torch.full((g.m_l, g.k_l), float("nan"), dtype=dtype, device="cuda")
-    dW = torch.full((g.what_len,), float("nan"), dtype=dtype, device="cuda")
+    dW = torch.full((g.what_len,), float("nan"), dtype=gdtype, device="cuda")
     fused = [ax.axonn_fc_output_buffer(h, w) for w in range(3)]
     outs = [O, dI, dW]
     if zero_copy:   # write straight into the handle-owned symmetric buffers
@@ -68,7 +75,7 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_co
     for w, shape in ((0, O.shape), (1, dI.shape), (2, dW.shape)):
         if zero_copy and fused[w]:   # read the symmetric buffer back into the tensor
             n_el = int(np.prod(shape))
-            src = torch.empty(n_el, dtype=dtype, device="cuda")
+            src = torch.empty(n_el, dtype=gdtype if w == 2 else dtype, device="cuda")
             import ctypes
             ctypes.CDLL("libcudart.so.12").cudaMemcpy(ctypes.c_void_p(src.data_ptr()),
                                                       ctypes.c_void_p(fused[w]),
@@ -85,8 +92,10 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_co
     dIg = np.full((m, k), np.nan)
     dWg = np.full((k, n), np.nan)
     L = pm.Layer(m, k, n, transposed)
-    eq = pm.layer_bytes(L, cfg, b=2 if dt == ax.AXONN_BF16 else 4)
-    tag = f"cfg={cfg} shape={(m, k, n)} T={transposed} {kind}/{dtype} chunks={chunks}"
+    eq = pm.layer_bytes(L, cfg, b=4 if dt == ax.AXONN_F32 else 2,
+                        b_grad=2 if dt == ax.AXONN_BF16 else 4)
+    tag = (f"cfg={cfg} shape={(m, k, n)} T={transposed} {kind}/{dtype}"
+           f"{'/gradf32' if grad_f32 else ''} chunks={chunks}")
     for r, (gg, o, di, dw, snt, _) in enumerate(allv):
         gg = ax.Geometry(*gg)
         for dst, val, r0, c0 in ((Og, o, gg.row0, gg.out_col0), (dIg, di, gg.row0, gg.in_col0)):
@@ -108,7 +117,7 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_co
                 assert snt[key] == v, f"bytes {key}: {snt} != Eq. {want} ({tag})"
     for name, got, ref in (("O", Og, O_ref), ("dI", dIg, dI_ref), ("dW", dWg, dW_ref)):
         assert not np.isnan(got).any(), f"{name} not fully covered: {tag}"
-        if kind == "int" and dtype == torch.float32:
+        if kind == "int" and (dtype == torch.float32 or (grad_f32 and name == "dW")):
             assert np.array_equal(got, ref), f"{name} not bit-exact: {tag}"
         else:
             err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
@@ -146,6 +155,9 @@ def main():
                     results[(fused, m, k, n, transposed)] = run_case(
                         cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank, world)
                     if fused == "red":
+                        # fp32 gradients: NCCL fp32 RS_z / AR_data beside fused bf16 AR_x/y
+                        run_case(cfg, m, k, n, transposed, "int", torch.bfloat16, 1, rank, world,
+                                 grad_f32=True)
                         zc = run_case(cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank,
                                       world, zero_copy=True)
                         if rank == 0:

@@ -88,6 +88,20 @@ def test_grid_select_matches_oracle(G, g_node, h, phase, gd):
             assert r[key] == pytest.approx(float(t[ok]), rel=1e-12, abs=0)
 
 
+@pytest.mark.parametrize("G,gd", [(8, 0), (16, 2), (64, 0)])
+def test_grid_select_mp_matches_oracle(G, gd):
+    layers = pm.gpt_block(6144, 16384, "fwd")
+    tb = _table(8)
+    want = pm.rank_configs(layers, G, 8, tb, 25e9, b=2, fixed_gd=gd, b_grad=4)
+    got = ax.axonn_grid_select([(L.m, L.k, L.n, L.transposed) for L in layers], G, 8, tb,
+                               25e9, 2, gd, grad_bytes_per_elem=4)
+    assert [(r["gx"], r["gy"], r["gz"], r["gd"]) for r in got] == [c for c, _ in want]
+    for r, (_, t) in zip(got, want):
+        for key, ok in (("t_ag_z", "ag_z"), ("t_rs_z", "rs_z"), ("t_ar_y", "ar_y"),
+                        ("t_ar_x", "ar_x"), ("t_ar_data", "ar_d"), ("t_comm", "comm")):
+            assert r[key] == pytest.approx(float(t[ok]), rel=1e-12, abs=0)
+
+
 def test_grid_select_errors():
     L = [(3, 5, 7, False)]
     with pytest.raises(ax.AxonnError) as e:

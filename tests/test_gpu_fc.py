@@ -21,10 +21,12 @@ def ax():
     yield ax
 
 
-def _layer(ax, m, k, n, transposed, kind, dtype_t, layer_id=0):
+def _layer(ax, m, k, n, transposed, kind, dtype_t, layer_id=0, grad_f32=False):
     torch = require_cuda()
     X, W, dY = synthdata.layer_tensors(m, k, n, layer_id, kind=kind)
     dt = ax.AXONN_F32 if dtype_t == torch.float32 else ax.AXONN_BF16
+    if grad_f32:
+        dt = ax.AXONN_BF16_GRADF32
     h = ax.axonn_fc_create(m, k, n, transposed, dt)
     g = ax.axonn_fc_geometry(h)
     assert (g.m_l, g.k_l, g.n_l, g.what_len) == (m, k, n, k * n)
@@ -33,7 +35,7 @@ def _layer(ax, m, k, n, transposed, kind, dtype_t, layer_id=0):
     dO = to_dev(dY, dtype_t)
     O = empty_dev(m, n, dtype_t)
     dI = empty_dev(m, k, dtype_t)
-    dW = empty_dev(1, k * n, dtype_t).reshape(-1)
+    dW = empty_dev(1, k * n, torch.float32 if grad_f32 else dtype_t).reshape(-1)
     ax.axonn_fc_forward(h, I, What, O)
     ax.axonn_fc_backward(h, dO, dI, dW)
     ax.axonn_grads_sync()
@@ -65,6 +67,32 @@ def test_f32_mode_bit_exact(ax):
     (X, W, dY), outs = _layer(ax, 192, 96, 160, False, "int", torch.float32)
     for got, ref in zip(outs, fc.fc_layer(X, W, dY)):
         np.testing.assert_array_equal(to_host_f64(got), ref)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+@pytest.mark.parametrize("m,k,n", [(256, 512, 1024), (384, 200, 136), (129, 96, 520)])
+def test_grad_f32_integer_bit_exact(ax, m, k, n, transposed):
+    """AXONN_BF16_GRADF32 (reading R17): O and dI as in bf16 mode, dŴ the
+    unrounded fp32 sum — exact on integer inputs."""
+    torch = require_cuda()
+    (X, W, dY), (O, dI, dW) = _layer(ax, m, k, n, transposed, "int", torch.bfloat16,
+                                     grad_f32=True)
+    rO, rI, rW = fc.fc_layer(X, W, dY)
+    for got, ref in ((O, rO), (dI, rI)):
+        assert np.array_equal(bf16_bits_of(got), synthdata.bf16_bits(synthdata.bf16_round(ref)))
+    assert dW.dtype == torch.float32
+    np.testing.assert_array_equal(to_host_f64(dW), rW)
+
+
+def test_grad_f32_random_beats_bf16_rounding(ax):
+    torch = require_cuda()
+    m, k, n = 2048, 1024, 768
+    (X, W, dY), (O, dI, dW) = _layer(ax, m, k, n, False, "uniform", torch.bfloat16,
+                                     grad_f32=True)
+    rW = fc.fc_backward_weight(X, dY)
+    absW = fc.fc_backward_weight(np.abs(X), np.abs(dY))
+    u = 2.0 ** -24
+    assert np.all(np.abs(to_host_f64(dW) - rW) <= m * u / (1 - m * u) * absW)
 
 
 def test_backward_before_forward_is_state_error(ax):

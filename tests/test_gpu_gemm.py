@@ -39,21 +39,25 @@ def _oracle(op, A, B):
     return fc.fc_backward_weight(A, B)         # I^T x dO
 
 
-def _run(op, A, B, M, N, dtype, pad=0):
+def _run(op, A, B, M, N, dtype, pad=0, out_f32=False, ldc=None):
+    """out_f32: bf16 operands, fp32 C (AXONN_BF16_GRADF32, the dW product of
+    fp32 gradient reduction)."""
     torch = require_cuda()
     import paper_2502_08145_b200 as ax
     lda = round_up(A.shape[1]) + pad
     ldb = round_up(B.shape[1]) + pad
-    ldc = round_up(N) + pad
+    ldc = (round_up(N) + pad) if ldc is None else ldc
     dA = to_dev(A, dtype, lda)
     dB = to_dev(B, dtype, ldb)
+    cdt = torch.float32 if out_f32 else dtype
     # output inside a NaN canary: 40 extra rows and the ld padding must stay NaN
     # (compute-sanitizer is closed on this pool; this is our out-of-bounds check)
-    guard = torch.full((M + 40, max(ldc, 1)), float("nan"), dtype=dtype, device="cuda")
+    guard = torch.full((M + 40, max(ldc, 1)), float("nan"), dtype=cdt, device="cuda")
     dC = guard[:M, :N]
     K = A.shape[0] if op == "TN" else A.shape[1]
-    ax.axonn_gemm(OPS[op], ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16,
-                  M, N, K, dA, lda, dB, ldb, dC, ldc)
+    code = (ax.AXONN_BF16_GRADF32 if out_f32 else
+            ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16)
+    ax.axonn_gemm(OPS[op], code, M, N, K, dA, lda, dB, ldb, dC, ldc)
     torch.cuda.synchronize()
     assert torch.isnan(guard[M:, :].float()).all(), "write below the last row"
     if ldc > N:
@@ -99,6 +103,62 @@ def test_f32_mode(op, M, N, K):
     A, B = _operands(op, M, N, K, "uniform")
     ref = _oracle(op, A, B)
     assert normwise_err(to_host_f64(_run(op, A, B, M, N, torch.float32)), ref) <= 1e-5
+
+
+# ---- fp32 output of the dW product (AXONN_BF16_GRADF32, reading R17) ----
+@pytest.mark.parametrize("M,N,K", SHAPES + [(256, 132, 512), (512, 260, 96)])
+def test_tn_fp32_output_integer_bit_exact(M, N, K):
+    """The unrounded fp32 accumulator: exact integers (|sum| <= 16 K < 2^24)."""
+    torch = require_cuda()
+    A, B = _operands("TN", M, N, K, "int")
+    got = to_host_f64(_run("TN", A, B, M, N, torch.bfloat16, out_f32=True))
+    np.testing.assert_array_equal(got, _oracle("TN", A, B))
+
+
+@pytest.mark.parametrize("M,N,K,ldc", [(384, 768, 320, None), (300, 520, 200, 524),
+                                       (257, 129, 65, 129), (2048, 1536, 1024, None)])
+def test_tn_fp32_output_random_within_gamma_bound(M, N, K, ldc):
+    """fp32 accumulation of exact bf16 products in any order: |got - ref| <=
+    gamma_K * sum|a||b| with gamma_K = K u / (1 - K u), u = 2^-24 (the
+    standard dot-product bound).  ldc 524 = padded rows (per-thread vector
+    stores), 129 = odd rows (scalar stores); None = TMA-store epilogue."""
+    torch = require_cuda()
+    A, B = _operands("TN", M, N, K, "uniform")
+    ref = _oracle("TN", A, B)
+    absref = _oracle("TN", np.abs(A), np.abs(B))
+    got = to_host_f64(_run("TN", A, B, M, N, torch.bfloat16, out_f32=True, ldc=ldc))
+    u = 2.0 ** -24
+    gamma = K * u / (1 - K * u)
+    assert np.all(np.abs(got - ref) <= gamma * absref)
+    # and strictly better than the bf16-output product
+    assert normwise_err(got, ref) <= 1e-5
+
+
+def test_tn_fp32_output_full_size_sampled():
+    """BASELINE.json C2 fc2 dW shape (M=4h, N=h, K=16384 tokens) in fp32."""
+    torch = require_cuda()
+    M, N, K = 16384, 4096, 16384
+    A, B = _operands("TN", M, N, K, "uniform")
+    C = _run("TN", A, B, M, N, torch.bfloat16, out_f32=True)
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, M, 4096)
+    cols = rng.integers(0, N, 4096)
+    ref = fc.dot_entries(A.T, B, rows, cols)
+    absref = fc.dot_entries(np.abs(A.T), np.abs(B), rows, cols)
+    got = C[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()].double().cpu().numpy()
+    u = 2.0 ** -24
+    assert np.all(np.abs(got - ref) <= K * u / (1 - K * u) * absref)
+
+
+@pytest.mark.parametrize("op", [0, 1])
+def test_fp32_output_only_for_tn(op):
+    torch = require_cuda()
+    import paper_2502_08145_b200 as ax
+    A = torch.zeros((64, 64), dtype=torch.bfloat16, device="cuda")
+    C = torch.zeros((64, 64), dtype=torch.float32, device="cuda")
+    with pytest.raises(ax.AxonnError) as e:
+        ax.axonn_gemm(op, ax.AXONN_BF16_GRADF32, 64, 64, 64, A, 64, A, 64, C, 64)
+    assert e.value.status == ax.AXONN_ERR_ARG and "TN" in str(e.value)
 
 
 @pytest.mark.parametrize("op", list(OPS))

@@ -162,3 +162,21 @@ def test_shape_errors_name_the_axis():
         alg1.check_shape(7, 8, 8, (1, 1, 2, 1))
     with pytest.raises(ValueError, match="Gx"):
         alg1.check_shape(8, 5, 8, (2, 1, 1, 1), transposed=True)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+def test_mixed_precision_bytes_equal_eqs_1_to_5(transposed):
+    # reading R17: weights and activations move in bf16 (b = 2 in Eqs. 1, 3,
+    # 4), the gradient reductions RS_z and AR_data in fp32 (b = 4 in Eqs. 2, 5)
+    m, k, n = 64, 32, 64
+    X, W, dO = synthdata.layer_tensors(m, k, n)
+    L = perf_model.Layer(m, k, n, transposed)
+    for cfg in [(1, 1, 2, 2), (2, 1, 2, 2), (1, 2, 4, 2), (1, 1, 1, 8), (1, 1, 8, 1)]:
+        res = alg1.simulate(X, W, dO, cfg, transposed)
+        eq = perf_model.layer_bytes(L, cfg, b=2, b_grad=4)
+        for r in range(cfg[0] * cfg[1] * cfg[2] * cfg[3]):
+            assert alg1.bytes_sent(res, "ag_z", r, 2) == eq["ag_z"]
+            assert alg1.bytes_sent(res, "ar_fwd", r, 2) == eq["ar_y"]
+            assert alg1.bytes_sent(res, "ar_bwd", r, 2) == eq["ar_x"]
+            assert alg1.bytes_sent(res, "rs_z", r, 4) == eq["rs_z"]
+            assert alg1.bytes_sent(res, "ar_d", r, 4) == eq["ar_d"]

@@ -131,3 +131,29 @@ def test_table3_efficiency_arithmetic():
         e = flops.efficiency(pf * 1e15, gpus, pk["advertised"] * 1e12, pk["empirical"] * 1e12)
         assert abs(e["pct_advertised"] - adv) <= 0.2, (system, gpus)
         assert abs(e["pct_empirical"] - emp) <= 0.2, (system, gpus)
+
+
+def test_mixed_precision_hand_values():
+    # Eqs. 2 and 5 with b = 4 on a layer small enough to do by hand:
+    # k = n = 8, Gz = Gd = 2, Gx = Gy = 1, m = 8.
+    #   Eq. 2: (Gz-1)/Gz * k n /(Gx Gy) * 4       = 1/2 * 64 * 4        = 128
+    #   Eq. 5: 2 (Gd-1)/Gd * k n /(Gx Gy Gz) * 4  = 2 * 1/2 * 32 * 4    = 128
+    #   Eq. 1 stays bf16: (Gz-1) * k n/(Gx Gy Gz) * 2 = 32 * 2          = 64
+    L = pm.Layer(8, 8, 8, False)
+    by = pm.layer_bytes(L, (1, 1, 2, 2), b=2, b_grad=4)
+    assert by["rs_z"] == 128 and by["ar_d"] == 128 and by["ag_z"] == 64
+    assert by["ar_y"] == 0 and by["ar_x"] == 0
+    # b_grad = b is the paper's single-precision form
+    assert pm.layer_bytes(L, (1, 1, 2, 2), b=2, b_grad=2) == pm.layer_bytes(L, (1, 1, 2, 2), b=2)
+
+
+def test_fp32_gradients_shift_the_ranking_toward_tensor_parallelism():
+    # doubling only the gradient bytes makes Z/DATA (whose cost is all
+    # gradient for DATA, half for Z) relatively dearer: the all-DATA config
+    # never improves its rank
+    layers = pm.gpt_block(4096, 16384, "fwd")
+    tb = pm.uniform_table(8, GB)
+    r2 = [c for c, _ in pm.rank_configs(layers, 8, 8, tb, GB, b=2)]
+    r4 = [c for c, _ in pm.rank_configs(layers, 8, 8, tb, GB, b=2, b_grad=4)]
+    assert sorted(r2) == sorted(r4)
+    assert r4.index((1, 1, 1, 8)) >= r2.index((1, 1, 1, 8))
