@@ -18,8 +18,16 @@ m = 16,384 N) on the grid the paper's performance model ranks first
 value = model flops of the step (6 m k n per layer, PAPER.md:786-795,
 SPEC.md:443) summed over ranks / device time of the step (CUDA events on the
 launching stream, max over ranks), in TFLOP/s.  e2e = the same metric with the
-per-step inputs (I and dO of every layer) copied host->device from pinned
-memory and the weight gradients read back, inside the timed region.
+per-step inputs copied host->device from pinned memory and the weight
+gradients read back, inside the timed region.  The block is chained the way
+the paper's alternating transposed layers allow: proj's
+output shard IS fc1's input shard and fc1's output shard IS fc2's (no
+communication between them), and in backward fc2's dI is fc1's dO and fc1's
+dI is proj's dO.  The step's external inputs are therefore the block input X
+(QKV), the attention output (proj's input; attention is outside the FC path),
+the loss gradient at fc2's output and attention-backward's gradient at QKV's
+output.  --no-chain runs the four layers on independent inputs instead (and
+then e2e uploads every layer's I and dO).
 --impl reference times the CPU fp64 oracle (oracle/) on a bounded sample.
 """
 from __future__ import annotations
@@ -235,6 +243,8 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="capture one step in a CUDA graph and time its replays")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="independent per-layer inputs (default: proj->fc1->fc2 chained)")
     args = ap.parse_args()
     # Exactly one JSON line on stdout: libraries (NCCL prints its version line)
     # write to fd 1, so fd 1 is pointed at stderr and the JSON goes to a copy.
@@ -281,18 +291,21 @@ def main():
     gen.manual_seed(42 + rank)
     bf = torch.bfloat16
 
-    def rnd(*shape):
+    def rnd(*shape, scale=1.0):
         t = torch.empty(shape, dtype=torch.float32, device="cuda")
-        t.uniform_(-1.0, 1.0, generator=gen)
+        t.uniform_(-scale, scale, generator=gen)
         return t.to(bf)
 
+    chain = not args.no_chain
     L = []
     for (mm, k, n, t) in layers:
         hd = ax.axonn_fc_create(mm, k, n, t, ax.AXONN_BF16, args.chunks)
         g = ax.axonn_fc_geometry(hd)
-        rec = {"h": hd, "g": g, "I": rnd(g.m_l, g.k_l), "W": rnd(g.what_len),
+        # random-init weights, variance preserving (U(+-sqrt(3/k)): unit-variance
+        # outputs for unit-variance inputs), so chained activations stay O(1)
+        rec = {"h": hd, "g": g, "W": rnd(g.what_len, scale=(3.0 / k) ** 0.5),
                "O": torch.empty(g.m_l, g.n_l, dtype=bf, device="cuda"),
-               "dO": rnd(g.m_l, g.n_l), "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
+               "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
                "dW": torch.empty(g.what_len, dtype=bf, device="cuda")}
         # outputs of fused (NVLS) all-reduces live in handle-owned symmetric
         # buffers; writing there avoids the final copy (include/axonn.h)
@@ -301,6 +314,22 @@ def main():
             if ptr:
                 rec[key] = ptr
         L.append(rec)
+    # inputs: external (uniform(-1,1), uploaded by e2e) or chained
+    ext_I, ext_dO = ([0, 1], [3, 0]) if chain else (list(range(4)), list(reversed(range(4))))
+    for i, l in enumerate(L):
+        g = l["g"]
+        if i in ext_I:
+            l["I"] = rnd(g.m_l, g.k_l)
+        else:
+            # a transposed layer's input shard is the previous
+            # (normal) layer's output shard and vice versa — same rows, same columns
+            p = L[i - 1]["g"]
+            assert (p.m_l, p.row0, p.n_l, p.out_col0) == (g.m_l, g.row0, g.k_l, g.in_col0), (p, g)
+            l["I"] = L[i - 1]["O"]
+        if i in ext_dO:
+            l["dO"] = rnd(g.m_l, g.n_l)
+        else:
+            l["dO"] = L[i + 1]["dI"]
 
     def step(s):
         for i, l in enumerate(L):
@@ -382,31 +411,34 @@ def main():
     # ---------------------------------------------------------------- e2e
     e2e = None
     if not args.no_e2e:
-        # Host buffers: each step uploads every layer's I and dO (pinned) and
-        # reads every dW back.  Device inputs are double-buffered so step s+1's
-        # uploads (copy stream, in consumption order) overlap step s's compute;
-        # read-backs run on a third stream (PCIe is full duplex).
-        hI = [l["I"].cpu().pin_memory() for l in L]
-        hdO = [l["dO"].cpu().pin_memory() for l in L]
+        # Host buffers: each step uploads the block's external inputs (pinned;
+        # with --no-chain every layer's I and dO) and reads every dW back.
+        # Device inputs are double-buffered so step s+1's uploads (copy stream,
+        # in consumption order) overlap step s's compute; read-backs run on a
+        # third stream (PCIe is full duplex).
+        hI = {i: L[i]["I"].cpu().pin_memory() for i in ext_I}
+        hdO = {i: L[i]["dO"].cpu().pin_memory() for i in ext_dO}
         hdW = [torch.empty(l["g"].what_len, dtype=bf).pin_memory() for l in L]
         dev_sets = [[(l["I"], l["dO"]) for l in L],
-                    [(torch.empty_like(l["I"]), torch.empty_like(l["dO"])) for l in L]]
+                    [(torch.empty_like(L[i]["I"]) if i in ext_I else L[i]["I"],
+                      torch.empty_like(L[i]["dO"]) if i in ext_dO else L[i]["dO"])
+                     for i in range(len(L))]]
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
         evI = [[torch.cuda.Event() for _ in L] for _ in range(2)]
         evO = [[torch.cuda.Event() for _ in L] for _ in range(2)]
         ev_free = [torch.cuda.Event(), torch.cuda.Event()]
         ev_done = torch.cuda.Event()
-        bi = sum(t.numel() * 2 for t in hI + hdO)
+        bi = sum(t.numel() * 2 for t in list(hI.values()) + list(hdO.values()))
         bo = sum(t.numel() * 2 for t in hdW)
 
         def upload(s_idx):
             b = s_idx % 2
             with torch.cuda.stream(up):
                 up.wait_event(ev_free[b])             # compute of step s-2 done with set b
-                for i in range(len(L)):
+                for i in ext_I:
                     dev_sets[b][i][0].copy_(hI[i], non_blocking=True)
                     evI[b][i].record(up)
-                for i in reversed(range(len(L))):
+                for i in ext_dO:
                     dev_sets[b][i][1].copy_(hdO[i], non_blocking=True)
                     evO[b][i].record(up)
 
@@ -414,12 +446,14 @@ def main():
             b = s_idx % 2
             with torch.cuda.stream(stream):
                 for i, l in enumerate(L):
-                    stream.wait_event(evI[b][i])
+                    if i in ext_I:
+                        stream.wait_event(evI[b][i])
                     ax.axonn_fc_forward(l["h"], dev_sets[b][i][0], l["W"], l["O"], stream)
                     if i + 1 < len(L):
                         ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
                 for i in reversed(range(len(L))):
-                    stream.wait_event(evO[b][i])
+                    if i in ext_dO:
+                        stream.wait_event(evO[b][i])
                     ax.axonn_fc_backward(L[i]["h"], dev_sets[b][i][1], L[i]["dI"], L[i]["dW"], stream)
                 ax.axonn_grads_sync(stream)
                 ev_free[b].record(stream)
@@ -457,6 +491,9 @@ def main():
         e2e = {"value": flops_step / (te * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world,
                "ms_per_step": te, "steps": ksteps,
+               "inputs": ("block input X, attention output (proj input), loss gradient at fc2 "
+                          "output, attention-backward gradient at QKV output; proj->fc1->fc2 chained "
+                          "on device (PAPER.md:402-414)") if chain else "every layer's I and dO",
                "path": "pinned host -> device uploads (double-buffered, copy stream) + "
                        "axonn_fc_forward/backward + grads_sync + dW device->host (third stream),"
                        " all inside the timed region"}
@@ -465,9 +502,10 @@ def main():
     exposed = None
     if world > 1:
         scratch = []
-        for l in L:
+        for l, (_, k_glob, _, _) in zip(L, layers):
             g = l["g"]
-            scratch.append((g, torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda").uniform_(-1, 1),
+            a = (3.0 / k_glob) ** 0.5   # same weight distribution as the Alg. 1 step
+            scratch.append((g, torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda").uniform_(-a, a),
                             torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda")))
 
         def gemm_step(s):
@@ -546,8 +584,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (uniform(-1,1) bf16, device-generated, seeded)",
-            "config": workload_config(args.model, world, grid, args.tokens_per_gpu),
+            "data": "synthetic (inputs uniform(-1,1) bf16, weights U(+-sqrt(3/k)) random init, "
+                    "device-generated, seeded)",
+            "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu),
+                       "chained": chain},
             "per_gpu_tflops": value / world,
             "frac_of_peak": {"advertised_2250": value / world / 2250.0,
                              "measured_burst": value / world / burst,

@@ -127,6 +127,70 @@ def run_case(cfg, m, k, n, transposed, kind, dtype, chunks, rank, world, zero_co
     return Og, dIg, dWg
 
 
+def run_chain(cfg, kind, dtype, rank):
+    """A normal layer feeding a transposed one, through the
+    ABI with no redistribution: layer 2's I_local IS layer 1's O_local buffer,
+    layer 1's dO_local IS layer 2's dI_local.  Each rank checks its own shards
+    against the composed fp64 network (fp32 + integers: bit-exact, all sums
+    < 2^24; bf16: normwise <= 2e-2 per shard)."""
+    m, k, hdim, n = 256, 128, 256, 128
+    X = synthdata.tensor((m, k), 301, kind=kind)
+    W1 = synthdata.tensor((k, hdim), 302, kind=kind)
+    W2 = synthdata.tensor((hdim, n), 303, kind=kind)
+    dY = synthdata.tensor((m, n), 304, kind=kind)
+    dt = ax.AXONN_F32 if dtype == torch.float32 else ax.AXONN_BF16
+    h1 = ax.axonn_fc_create(m, k, hdim, False, dt)
+    h2 = ax.axonn_fc_create(m, hdim, n, True, dt)
+    g1, g2 = ax.axonn_fc_geometry(h1), ax.axonn_fc_geometry(h2)
+    assert (g1.m_l, g1.row0, g1.n_l, g1.out_col0) == (g2.m_l, g2.row0, g2.k_l, g2.in_col0)
+
+    def what(W, g):
+        Wl = np.ascontiguousarray(W[g.in_col0:g.in_col0 + g.k_l, g.out_col0:g.out_col0 + g.n_l])
+        return dev(Wl.reshape(1, -1)[:, g.what_off:g.what_off + g.what_len], dtype).reshape(-1)
+
+    I1 = dev(X[g1.row0:g1.row0 + g1.m_l, g1.in_col0:g1.in_col0 + g1.k_l], dtype)
+    dO2 = dev(dY[g2.row0:g2.row0 + g2.m_l, g2.out_col0:g2.out_col0 + g2.n_l], dtype)
+    Wh1, Wh2 = what(W1, g1), what(W2, g2)
+    O1 = torch.empty((g1.m_l, g1.n_l), dtype=dtype, device="cuda")
+    O2 = torch.empty((g2.m_l, g2.n_l), dtype=dtype, device="cuda")
+    dI2 = torch.empty((g2.m_l, g2.k_l), dtype=dtype, device="cuda")
+    dI1 = torch.empty((g1.m_l, g1.k_l), dtype=dtype, device="cuda")
+    dW1 = torch.empty((g1.what_len,), dtype=dtype, device="cuda")
+    dW2 = torch.empty((g2.what_len,), dtype=dtype, device="cuda")
+    s = torch.cuda.current_stream()
+    ax.axonn_fc_forward(h1, I1, Wh1, O1, s)
+    ax.axonn_fc_forward(h2, O1, Wh2, O2, s)          # chained: no redistribution
+    ax.axonn_fc_backward(h2, dO2, dI2, dW2, s)
+    ax.axonn_fc_backward(h1, dI2, dI1, dW1, s)       # chained
+    ax.axonn_grads_sync(s)
+    torch.cuda.synchronize()
+    ax.axonn_fc_destroy(h1)
+    ax.axonn_fc_destroy(h2)
+    # composed network, fp64 (oracle.fc)
+    rO1 = fc.fc_forward(X, W1)
+    rO2 = fc.fc_forward(rO1, W2)
+    rdO1 = fc.fc_backward_input(dY, W2)
+    rdW2 = fc.fc_backward_weight(rO1, dY)
+    rdX = fc.fc_backward_input(rdO1, W1)
+    rdW1 = fc.fc_backward_weight(X, rdO1)
+
+    def flat_slice(R, g):
+        return np.ascontiguousarray(R[g.in_col0:g.in_col0 + g.k_l, g.out_col0:g.out_col0 + g.n_l]
+                                    ).reshape(-1)[g.what_off:g.what_off + g.what_len]
+
+    checks = (("O2", host(O2), rO2[g2.row0:g2.row0 + g2.m_l, g2.out_col0:g2.out_col0 + g2.n_l]),
+              ("dX", host(dI1), rdX[g1.row0:g1.row0 + g1.m_l, g1.in_col0:g1.in_col0 + g1.k_l]),
+              ("dW1", host(dW1), flat_slice(rdW1, g1)), ("dW2", host(dW2), flat_slice(rdW2, g2)))
+    for name, got, ref in checks:
+        if kind == "int" and dtype == torch.float32:
+            assert np.array_equal(got, ref), f"chain {name} not bit-exact cfg={cfg} rank {rank}"
+        else:
+            err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
+            assert err <= 2e-2, f"chain {name} normwise {err} cfg={cfg} rank {rank}"
+    if rank == 0:
+        print(f"ok chain N->T cfg={cfg} {kind}/{dtype}", flush=True)
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -163,7 +227,9 @@ def main():
                         if rank == 0:
                             for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
                                 assert np.array_equal(a, b), f"zero-copy differs {cfg}"
+            run_chain(cfg, "uniform", torch.bfloat16, rank)
             if fused == "0":
+                run_chain(cfg, "int", torch.float32, rank)
                 run_case(cfg, 512, 256, 512, False, "int", torch.float32, 3, rank, world)
                 run_case(cfg, 512, 256, 512, False, "uniform", torch.bfloat16, 3, rank, world)
             ax.axonn_grid_finalize()
