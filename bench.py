@@ -226,6 +226,30 @@ def workload_config(model, n, grid, tpg=16384):
             "l2": "no flush: per-step operands (>= 134 MB each for I/dO of the fc2 layer) exceed the 126 MB L2"}
 
 
+def bind_numa_local(device: int):
+    """Pin this rank's host threads to the CPUs NVML reports as local to its
+    GPU, before any pinned host buffer is allocated, so first-touch places the
+    e2e staging buffers on the GPU's NUMA node (a cross-socket hop halves
+    PCIe upload bandwidth when several ranks upload at once).  Returns the
+    CPU count bound to, or None if NVML cannot say."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(device)
+        pynvml.nvmlInit()
+        hnd = pynvml.nvmlDeviceGetHandleByPciBusId(
+            f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        words = pynvml.nvmlDeviceGetCpuAffinity(hnd, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, word in enumerate(words) for b in range(64) if word >> b & 1}
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return len(cpus)
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -243,6 +267,8 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="capture one step in a CUDA graph and time its replays")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--w-init", default="scaled", choices=["scaled", "uniform"],
+                    help="weights U(+-sqrt(3/k)) (random init) or U(-1,1)")
     ap.add_argument("--no-chain", action="store_true",
                     help="independent per-layer inputs (default: proj->fc1->fc2 chained)")
     args = ap.parse_args()
@@ -303,7 +329,8 @@ def main():
         g = ax.axonn_fc_geometry(hd)
         # random-init weights, variance preserving (U(+-sqrt(3/k)): unit-variance
         # outputs for unit-variance inputs), so chained activations stay O(1)
-        rec = {"h": hd, "g": g, "W": rnd(g.what_len, scale=(3.0 / k) ** 0.5),
+        wscale = (3.0 / k) ** 0.5 if args.w_init == "scaled" else 1.0
+        rec = {"h": hd, "g": g, "W": rnd(g.what_len, scale=wscale),
                "O": torch.empty(g.m_l, g.n_l, dtype=bf, device="cuda"),
                "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
                "dW": torch.empty(g.what_len, dtype=bf, device="cuda")}
@@ -411,6 +438,8 @@ def main():
     # ---------------------------------------------------------------- e2e
     e2e = None
     if not args.no_e2e:
+        cpus0 = os.sched_getaffinity(0)
+        numa_cpus = bind_numa_local(local)
         # Host buffers: each step uploads the block's external inputs (pinned;
         # with --no-chain every layer's I and dO) and reads every dW back.
         # Device inputs are double-buffered so step s+1's uploads (copy stream,
@@ -418,7 +447,18 @@ def main():
         # third stream (PCIe is full duplex).
         hI = {i: L[i]["I"].cpu().pin_memory() for i in ext_I}
         hdO = {i: L[i]["dO"].cpu().pin_memory() for i in ext_dO}
-        hdW = [torch.empty(l["g"].what_len, dtype=bf).pin_memory() for l in L]
+        # the step's result, the weight gradient, crosses to the host once:
+        # the Gd data-parallel replicas hold identical dŴ, so each reads back
+        # the 1/Gd slice its DATA coordinate selects (the union over ranks is
+        # every dŴ element exactly once)
+        _, _, _, dcoord = ax.axonn_grid_coords()
+        gd = grid[3]
+        wsl = []
+        for l in L:
+            S_ = l["g"].what_len
+            lo, hi = S_ * dcoord // gd, S_ * (dcoord + 1) // gd
+            wsl.append((lo, hi))
+        hdW = [torch.empty(hi - lo, dtype=bf).pin_memory() for lo, hi in wsl]
         dev_sets = [[(l["I"], l["dO"]) for l in L],
                     [(torch.empty_like(L[i]["I"]) if i in ext_I else L[i]["I"],
                       torch.empty_like(L[i]["dO"]) if i in ext_dO else L[i]["dO"])
@@ -428,8 +468,12 @@ def main():
         evO = [[torch.cuda.Event() for _ in L] for _ in range(2)]
         ev_free = [torch.cuda.Event(), torch.cuda.Event()]
         ev_done = torch.cuda.Event()
+        ev_read = [torch.cuda.Event() for _ in L]
         bi = sum(t.numel() * 2 for t in list(hI.values()) + list(hdO.values()))
         bo = sum(t.numel() * 2 for t in hdW)
+        # whole job: the slices' union is every weight-gradient element once
+        bo_total = sum(2 * k * n for (_, k, n, _) in layers)
+        assert world > 1 or bo == bo_total
 
         def upload(s_idx):
             b = s_idx % 2
@@ -454,17 +498,20 @@ def main():
                 for i in reversed(range(len(L))):
                     if i in ext_dO:
                         stream.wait_event(evO[b][i])
+                    stream.wait_event(ev_read[i])    # previous step's dŴ has reached the host
                     ax.axonn_fc_backward(L[i]["h"], dev_sets[b][i][1], L[i]["dI"], L[i]["dW"], stream)
                 ax.axonn_grads_sync(stream)
                 ev_free[b].record(stream)
                 ev_done.record(stream)
             with torch.cuda.stream(down):
                 down.wait_event(ev_done)
-                for i, l in enumerate(L):
+                for i in reversed(range(len(L))):    # in the next step's backward order
+                    l = L[i]
                     if isinstance(l["dW"], int):
-                        copy_raw(hdW[i].data_ptr(), l["dW"], hdW[i].numel() * 2, down)
+                        copy_raw(hdW[i].data_ptr(), l["dW"] + 2 * wsl[i][0], hdW[i].numel() * 2, down)
                     else:
-                        hdW[i].copy_(l["dW"], non_blocking=True)
+                        hdW[i].copy_(l["dW"][wsl[i][0]:wsl[i][1]], non_blocking=True)
+                    ev_read[i].record(down)
 
         def e2e_run(n):
             upload(0)
@@ -489,8 +536,9 @@ def main():
         barrier()
         te = max_over_ranks(e0.elapsed_time(e1)) / ksteps
         e2e = {"value": flops_step / (te * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world,
+               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo_total,
                "ms_per_step": te, "steps": ksteps,
+               "numa_local_cpus": numa_cpus,
                "inputs": ("block input X, attention output (proj input), loss gradient at fc2 "
                           "output, attention-backward gradient at QKV output; proj->fc1->fc2 chained "
                           "on device (PAPER.md:402-414)") if chain else "every layer's I and dO",
@@ -498,13 +546,15 @@ def main():
                        "axonn_fc_forward/backward + grads_sync + dW device->host (third stream),"
                        " all inside the timed region"}
 
+        os.sched_setaffinity(0, cpus0)   # the CPU baseline below uses every core
+
     # ---------------------------------------------------------------- GEMM-only (exposed comm)
     exposed = None
     if world > 1:
         scratch = []
         for l, (_, k_glob, _, _) in zip(L, layers):
             g = l["g"]
-            a = (3.0 / k_glob) ** 0.5   # same weight distribution as the Alg. 1 step
+            a = (3.0 / k_glob) ** 0.5 if args.w_init == "scaled" else 1.0  # as the Alg. 1 step
             scratch.append((g, torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda").uniform_(-a, a),
                             torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda")))
 
@@ -584,8 +634,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (inputs uniform(-1,1) bf16, weights U(+-sqrt(3/k)) random init, "
-                    "device-generated, seeded)",
+            "data": ("synthetic (inputs uniform(-1,1) bf16, weights "
+                     + ("U(+-sqrt(3/k)) random init" if args.w_init == "scaled" else "U(-1,1)")
+                     + ", device-generated, seeded)"),
             "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu),
                        "chained": chain},
             "per_gpu_tflops": value / world,
