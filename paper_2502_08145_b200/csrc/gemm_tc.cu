@@ -288,6 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                            const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmC, int use_tma_store,
                            void* __restrict__ Cv, int64_t ldc, int M, int N, int K,
+                           int split_release,
                            int group_m, const __grid_constant__ EpiTarget epi,
                            int* __restrict__ tile_counter) {
   using Cfg = PairCfg<MT>;
@@ -425,35 +426,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      // the K-block `kb` staged in slot `st`, sub-tiles [mt0, mt1) of the accumulator
+      auto issue = [&](uint32_t d_tmem, int st, int kb, int mt0, int mt1) {
+        const uint32_t a_base = ptx::smem_u32(sA + st * Cfg::SMEM_A);
+        const uint32_t b_base = ptx::smem_u32(sB + st * Cfg::SMEM_B);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                   : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            if (mt < mt0 || mt >= mt1) continue;
+            // rows [mt*128, mt*128+128) of each CTA's A start 16 KiB apart in
+            // both majors (128 rows x 128 B, or two 8-KiB MN chunks)
+            const uint32_t ab = a_base + mt * 16384;
+            const uint64_t ad = A_MN ? ptx::sdesc_sw128(ab + kk * 2048, MN_CHUNK_BYTES, 1024)
+                                     : ptx::sdesc_sw128(ab + kk * 32, 16, 1024);
+            ptx::umma_f16_2sm(d_tmem + mt * Cfg::BN, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+        }
+      };
+      auto advance = [&](int& st, uint32_t& ph) {
+        if (++st == Cfg::STAGES) {
+          st = 0;
+          ph ^= 1;
+        }
+      };
       for (int seq = 0;; ++seq) {
         if (consume_tile(seq, true) < 0) break;
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-        ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * MT * Cfg::BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb = 0;
+        if (MT == 2) {
+          // One accumulator (all 512 columns), released per sub-tile: while the
+          // epilogue still drains sub-tile 1 of the previous tile, the first
+          // STAGES staged K-blocks already accumulate into sub-tile 0.
+          ptx::mbar_wait(&tempty[0], acc_phase ^ 1);
+          if (!split_release) ptx::mbar_wait(&tempty[1], acc_phase ^ 1);
+          ptx::tc_fence_after();
+          const int pro = !split_release ? 0 : num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES;
+          int st2 = stage;
+          uint32_t ph2 = phase;
+          for (int j = 0; j < pro; ++j) {
+            ptx::mbar_wait(&full[st2], ph2);
+            ptx::tc_fence_after();
+            issue(d_tmem, st2, j, 0, 1);
+            advance(st2, ph2);
+          }
+          if (split_release) {
+            ptx::mbar_wait(&tempty[1], acc_phase ^ 1);
+            ptx::tc_fence_after();
+          }
+          for (; kb < pro; ++kb) {
+            issue(d_tmem, stage, kb, 1, 2);
+            ptx::umma_commit_2sm(&empty[stage], 0x3);  // frees the slot in both CTAs
+            advance(stage, phase);
+          }
+        } else {
+          ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+          ptx::tc_fence_after();
+        }
+        for (; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_base = ptx::smem_u32(sA + stage * Cfg::SMEM_A);
-          const uint32_t b_base = ptx::smem_u32(sB + stage * Cfg::SMEM_B);
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, MN_CHUNK_BYTES, 1024)
-                                     : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-              // rows [mt*128, mt*128+128) of each CTA's A start 16 KiB apart in
-              // both majors (128 rows x 128 B, or two 8-KiB MN chunks)
-              const uint32_t ab = a_base + mt * 16384;
-              const uint64_t ad = A_MN ? ptx::sdesc_sw128(ab + kk * 2048, MN_CHUNK_BYTES, 1024)
-                                       : ptx::sdesc_sw128(ab + kk * 32, 16, 1024);
-              ptx::umma_f16_2sm(d_tmem + mt * Cfg::BN, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-            }
-          }
+          issue(d_tmem, stage, kb, 0, MT);
           ptx::umma_commit_2sm(&empty[stage], 0x3);  // frees the slot in both CTAs
-          if (++stage == Cfg::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          advance(stage, phase);
         }
         ptx::umma_commit_2sm(&tfull[acc], 0x3);      // both CTAs' accumulators ready
         if (++acc == Cfg::ACC) {
@@ -599,10 +636,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           }
           __syncwarp();
         }
+        if (MT == 2) {
+          // this warp's share of sub-tile mt is out of TMEM: release it (the
+          // MMA warp starts the next tile on sub-tile 0 before sub-tile 1 is free)
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_leader(&tempty[mt]);
+        }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+      if (MT != 2) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+      }
       if (++acc == Cfg::ACC) {
         acc = 0;
         acc_phase ^= 1;
@@ -717,8 +763,10 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   if (2 * tiles < grid) grid = 2 * tiles;
   if (grid < 2) grid = 2;
   int* counter = next_tile_counter(stream);
+  // MT=2: release the accumulator per sub-tile (AXONN_SPLIT_RELEASE=0: whole tile)
+  static const int split = env_int("AXONN_SPLIT_RELEASE", 1) != 0;
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
-                                                       group_m, epi, counter);
+                                                       split, group_m, epi, counter);
   return cudaGetLastError();
 }
 

@@ -212,11 +212,13 @@ def test_full_size_sampled(op, M, N, K):
 
 
 @pytest.mark.parametrize("env", [{"AXONN_GEMM_VARIANT": "single"}, {"AXONN_PAIR_MT": "1"},
-                                 {"AXONN_GROUP_M": "-8"}, {"AXONN_SCHED": "static"}])
+                                 {"AXONN_GROUP_M": "-8"}, {"AXONN_SCHED": "static"},
+                                 {"AXONN_SPLIT_RELEASE": "0"}])
 def test_alternative_kernel_configurations(env):
-    """The 1-CTA kernel, the 256x256 CTA-pair tile, the transposed raster and
-    static tile scheduling (selected by environment, read once per process)
-    pass the same bit-exact integer and full-size checks."""
+    """The 1-CTA kernel, the 256x256 CTA-pair tile, the transposed raster,
+    static tile scheduling and whole-tile accumulator release (selected by
+    environment, read once per process) pass the same bit-exact integer and
+    full-size checks."""
     import os
     import subprocess
     import sys
