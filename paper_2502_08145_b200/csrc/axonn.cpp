@@ -139,6 +139,24 @@ axonn_status_t ensure_device() {
 }
 
 
+// Events that order work ACROSS calls (ev_rsdone: the previous fused RS_z
+// owner phase; ev_wdone: the previous deferred data-parallel reduction).
+// Under stream capture they become external event nodes, so a graph replay
+// waits on the previous iteration's (or the eager run's) real record exactly
+// as eager execution does; a plain capture would reject the dependency on
+// uncaptured work (or drop it).
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive;
+}
+cudaError_t record_xcall(cudaEvent_t e, cudaStream_t st) {
+  return capturing(st) ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                       : cudaEventRecord(e, st);
+}
+cudaError_t wait_xcall(cudaStream_t st, cudaEvent_t e) {
+  return cudaStreamWaitEvent(st, e, capturing(st) ? cudaEventWaitExternal : 0);
+}
+
 // Per-rank bytes a ring collective sends (Assumption-1):
 // all-gather (p-1)*count, reduce-scatter (p-1)*recvcount, all-reduce
 // 2(p-1)/p*count — the quantities of Eqs. 1-5.
@@ -347,7 +365,9 @@ bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64
   f->epi = axonn::EpiTarget();
   const int P = S.g[axis];
   const int64_t n = rows * cols;
-  if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % 8) return true;  // NCCL path
+  // NCCL path: no window, a 1-rank axis, an empty output, 8-element rows not
+  // possible, or an empty product (K == 0 writes zeros; nothing to scatter)
+  if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % 8 || kdim <= 0) return true;
   const bool red = P == 2 && kdim >= env_int("AXONN_RED_MIN_K", 8192);
   if (!red && n % (8 * P)) return true;
   f->elems = static_cast<size_t>(n);
@@ -817,7 +837,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
   auto dW_gemm = [&]() -> axonn_status_t {
     if (fZ)  // the previous fused RS_z must have released every rank's slots
-      CUDA_TRY(cudaStreamWaitEvent(st, h->ev_rsdone, 0));
+      CUDA_TRY(wait_xcall(st, h->ev_rsdone));
     return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
                     st, fW ? &h->fw.epi : (fZ ? &h->fz.epi : nullptr));
   };
@@ -834,7 +854,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
                                        h->fz.epi.me, S.num_sms, zs, dW_hat));
       g_launches.fetch_add(1);
       STATUS_TRY(fused_barrier(AX_Z, zs));  // every owner is done with its slots
-      CUDA_TRY(cudaEventRecord(h->ev_rsdone, zs));
+      CUDA_TRY(record_xcall(h->ev_rsdone, zs));
       count_comm(1, S.g[AX_Z], S_el, dt);
       CUDA_TRY(cudaEventRecord(h->ev_grad, zs));
       last = h->ev_grad;
@@ -861,7 +881,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   // fused outputs: buffers ready on every rank before any rank's epilogue writes
   if (fI) STATUS_TRY(fused_pre(h->fi, st));
   if (fW) {
-    CUDA_TRY(cudaStreamWaitEvent(st, h->ev_wdone, 0));  // previous deferred reduction done
+    CUDA_TRY(wait_xcall(st, h->ev_wdone));  // previous deferred reduction done
     STATUS_TRY(fused_pre(h->fw, st));
   }
   if (Pb > 1 && !fI) {
@@ -904,7 +924,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     STATUS_TRY(fused_post(h->fw, ds, 1));
     if (dW_hat != h->fw.out.ptr)
       CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fw.out.ptr, S_el * es, cudaMemcpyDeviceToDevice, ds));
-    CUDA_TRY(cudaEventRecord(h->ev_wdone, ds));
+    CUDA_TRY(record_xcall(h->ev_wdone, ds));
     CUDA_TRY(cudaEventRecord(h->ev_grad, ds));
     last = h->ev_grad;
   }

@@ -191,6 +191,70 @@ def run_chain(cfg, kind, dtype, rank):
         print(f"ok chain N->T cfg={cfg} {kind}/{dtype}", flush=True)
 
 
+def run_graph(cfg, rank):
+    """One layer step (OAG prefetch, forward, backward, grads_sync) captured in a
+    CUDA graph — NCCL calls, device-side barriers, copy-engine gathers and the
+    library's cross-stream forks included — must reproduce the eager outputs
+    bit for bit on every replay."""
+    m, k, n = 256, 512, 1024
+    X, W, dY = synthdata.layer_tensors(m, k, n, 11)
+    h = ax.axonn_fc_create(m, k, n, False, ax.AXONN_BF16)
+    g = ax.axonn_fc_geometry(h)
+    I = dev(X[g.row0:g.row0 + g.m_l, g.in_col0:g.in_col0 + g.k_l], torch.bfloat16)
+    Wl = np.ascontiguousarray(W[g.in_col0:g.in_col0 + g.k_l, g.out_col0:g.out_col0 + g.n_l])
+    What = dev(Wl.reshape(1, -1)[:, g.what_off:g.what_off + g.what_len], torch.bfloat16).reshape(-1)
+    dO = dev(dY[g.row0:g.row0 + g.m_l, g.out_col0:g.out_col0 + g.n_l], torch.bfloat16)
+    outs = [torch.empty((g.m_l, g.n_l), dtype=torch.bfloat16, device="cuda"),
+            torch.empty((g.m_l, g.k_l), dtype=torch.bfloat16, device="cuda"),
+            torch.empty((g.what_len,), dtype=torch.bfloat16, device="cuda")]
+
+    def step(s):
+        ax.axonn_fc_prefetch(h, What, s)
+        ax.axonn_fc_forward(h, I, What, outs[0], s)
+        ax.axonn_fc_backward(h, dO, outs[1], outs[2], s)
+        ax.axonn_grads_sync(s)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(s)
+    torch.cuda.synchronize()
+    eager = [o.clone() for o in outs]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s, capture_error_mode="thread_local"):
+        step(s)
+    for rep in range(2):
+        for o in outs:
+            o.fill_(float("nan"))
+        dist.barrier()
+        graph.replay()
+        torch.cuda.synchronize()
+        for name, a, b in zip(("O", "dI", "dW"), outs, eager):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16)), \
+                f"graph replay {rep} {name} differs at cfg={cfg} rank {rank}"
+    del graph
+    ax.axonn_fc_destroy(h)
+    if rank == 0:
+        print(f"ok graph replay cfg={cfg}", flush=True)
+
+
+def run_empty(cfg, rank):
+    """m = 0 on every grid: no tokens -> O, dI empty; dŴ = 0 exactly."""
+    k, n = 128, 256
+    h = ax.axonn_fc_create(0, k, n, False, ax.AXONN_BF16)
+    g = ax.axonn_fc_geometry(h)
+    e = lambda *sh: torch.empty(sh, dtype=torch.bfloat16, device="cuda")  # noqa: E731
+    What = torch.ones((max(g.what_len, 1),), dtype=torch.bfloat16, device="cuda")
+    dW = torch.full((g.what_len,), float("nan"), dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.current_stream()
+    ax.axonn_fc_forward(h, e(0, g.k_l), What, e(0, g.n_l), s)
+    ax.axonn_fc_backward(h, e(0, g.n_l), e(0, g.k_l), dW, s)
+    ax.axonn_grads_sync(s)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(dW).item() == 0 and not torch.isnan(dW).any(), f"m=0 cfg={cfg}"
+    ax.axonn_fc_destroy(h)
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -228,6 +292,9 @@ def main():
                             for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
                                 assert np.array_equal(a, b), f"zero-copy differs {cfg}"
             run_chain(cfg, "uniform", torch.bfloat16, rank)
+            if fused in ("red", "0"):
+                run_graph(cfg, rank)
+                run_empty(cfg, rank)
             if fused == "0":
                 run_chain(cfg, "int", torch.float32, rank)
                 run_case(cfg, 512, 256, 512, False, "int", torch.float32, 3, rank, world)

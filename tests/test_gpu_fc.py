@@ -95,6 +95,25 @@ def test_grad_f32_random_beats_bf16_rounding(ax):
     assert np.all(np.abs(to_host_f64(dW) - rW) <= m * u / (1 - m * u) * absW)
 
 
+def test_zero_tokens(ax):
+    """m = 0 (an empty batch): O and dI are empty, dŴ = Xᵀ dY over no rows = 0."""
+    torch = require_cuda()
+    k, n = 256, 136
+    h = ax.axonn_fc_create(0, k, n)
+    W = torch.ones(k * n, dtype=torch.bfloat16, device="cuda")
+    I = torch.empty((0, k), dtype=torch.bfloat16, device="cuda")
+    dO = torch.empty((0, n), dtype=torch.bfloat16, device="cuda")
+    O = torch.empty((0, n), dtype=torch.bfloat16, device="cuda")
+    dI = torch.empty((0, k), dtype=torch.bfloat16, device="cuda")
+    dW = torch.full((k * n,), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ax.axonn_fc_forward(h, I, W, O)
+    ax.axonn_fc_backward(h, dO, dI, dW)
+    ax.axonn_grads_sync()
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(dW).item() == 0 and not torch.isnan(dW).any()
+    ax.axonn_fc_destroy(h)
+
+
 def test_backward_before_forward_is_state_error(ax):
     torch = require_cuda()
     h = ax.axonn_fc_create(128, 128, 128)
