@@ -50,7 +50,8 @@ typedef enum {
   AXONN_BF16_GRADF32 = 2      /* bf16 operands, activations and W; the weight gradient dŴ is
                                  fp32 (the dW product's accumulator is stored unrounded) and
                                  RS_z / the data-parallel all-reduce sum fp32 (b = 4 in
-                                 Eqs. 2, 5, reading R17)               */
+                                 Eqs. 2, 5, reading R17), fused over
+                                 NVLS like bf16 (scatter + fp32 owner phase) or NCCL fp32  */
 } axonn_dtype_t;
 
 /* Message of the last failing call on this thread ("" if none). Never NULL. */
@@ -143,7 +144,7 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
 
 /* Handle-owned output buffers of the fused GEMM + all-reduce path (B200
  * NVLS): which = 0 -> O_local, 1 -> dI_local, 2 -> dW_hat.  *ptr is NULL when
- * that output takes the NCCL path (fp32 mode, an fp32 dŴ, a row length
+ * that output takes the NCCL path (fp32 mode, a row length
  * not a multiple of 8, or AXONN_FUSED=0).  Passing the returned pointer as the
  * output argument of axonn_fc_forward / axonn_fc_backward avoids the final
  * device-to-device copy; its contents are valid until the next call that

@@ -321,6 +321,7 @@ struct axonn_fc {
   // fused all-reduces (epi.mode == kStore: NCCL path)
   struct Fused {
     int axis = 0;
+    int es = 2;                // element bytes: 2 (bf16), 4 (fp32 dŴ, AXONN_BF16_GRADF32)
     size_t elems = 0;
     void* out_peer = nullptr;  // 2-rank scatter mode: the peer's copy of our slice
     axonn::SymBuf out;    // every rank's result (handle-owned output buffer)
@@ -360,24 +361,27 @@ axonn_status_t fused_barrier(int axis, cudaStream_t st, int index) {
 // Shorter K (e.g. the transposed proj layer, K = h/Gx) uses the scatter mode,
 // whose epilogue traffic is half as large and goes out as plain stores.
 bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_t kdim,
-                 std::string* why) {
+                 std::string* why, int es = 2) {
   f->axis = axis;
+  f->es = es;
   f->epi = axonn::EpiTarget();
   const int P = S.g[axis];
   const int64_t n = rows * cols;
+  const int unit = 16 / es;  // elements per 16-B epilogue unit
   // NCCL path: no window, a 1-rank axis, an empty output, 8-element rows not
   // possible, or an empty product (K == 0 writes zeros; nothing to scatter)
-  if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % 8 || kdim <= 0) return true;
-  const bool red = P == 2 && kdim >= env_int("AXONN_RED_MIN_K", 8192);
-  if (!red && n % (8 * P)) return true;
+  if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % unit || kdim <= 0) return true;
+  // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
+  const bool red = es == 2 && P == 2 && kdim >= env_int("AXONN_RED_MIN_K", 8192);
+  if (!red && n % (unit * P)) return true;
   f->elems = static_cast<size_t>(n);
-  if (!axonn::sym_alloc(&S.sym[axis], f->elems * 2, &f->out, why)) return false;
+  if (!axonn::sym_alloc(&S.sym[axis], f->elems * es, &f->out, why)) return false;
   if (red) {
     f->epi.mode = axonn::kMcRed;
     f->epi.mc = reinterpret_cast<unsigned long long>(f->out.mc);
     return true;
   }
-  if (!axonn::sym_alloc(&S.sym[axis], f->elems * 2, &f->recv, why)) return false;
+  if (!axonn::sym_alloc(&S.sym[axis], f->elems * es, &f->recv, why)) return false;
   f->epi.mode = axonn::kScatter;
   f->epi.P = P;
   f->epi.me = S.c[axis];
@@ -395,7 +399,7 @@ bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64
       *why = "peer address of the output window unavailable";
       return false;
     }
-    f->out_peer = peer_out + static_cast<size_t>(f->epi.me) * f->epi.slice * 2;
+    f->out_peer = peer_out + static_cast<size_t>(f->epi.me) * f->epi.slice * es;
   }
   return true;
 }
@@ -405,7 +409,7 @@ axonn_status_t fused_barrier(int axis, cudaStream_t st, int index = 0);
 axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
   if (f.epi.mode == axonn::kMcRed) {
     // zero every rank's copy, and order that before any rank's reductions
-    CUDA_TRY(cudaMemsetAsync(f.out.ptr, 0, f.elems * 2, st));
+    CUDA_TRY(cudaMemsetAsync(f.out.ptr, 0, f.elems * f.es, st));
     return fused_barrier(f.axis, st);
   }
   return AXONN_OK;  // scatter: the previous use's final barrier already freed the slots
@@ -416,9 +420,9 @@ axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
   if (f.epi.mode == axonn::kScatter) {
     void* local = nullptr;
     if (f.out_peer)  // 2 ranks: own copy + plain stores to the peer instead of multicast
-      local = static_cast<char*>(f.out.ptr) + static_cast<size_t>(f.epi.me) * f.epi.slice * 2;
+      local = static_cast<char*>(f.out.ptr) + static_cast<size_t>(f.epi.me) * f.epi.slice * f.es;
     CUDA_TRY(axonn::sym_owner_reduce(&f.recv, &f.out, f.epi.slice, f.epi.P, f.epi.me, S.num_sms,
-                                     st, local, f.out_peer));
+                                     st, local, f.out_peer, f.es == 4));
     g_launches.fetch_add(1);
     STATUS_TRY(fused_barrier(f.axis, st, index));  // every owner's broadcast has landed
   }
@@ -651,21 +655,23 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
   if (desc->dtype != AXONN_F32) {
-    // the fused epilogues reduce bf16; an fp32 dŴ takes NCCL
+    // O and dI reduce bf16; dŴ in its gradient precision (fp32 for AXONN_BF16_GRADF32)
     std::string why;
     if (!fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, &why) ||
         !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, &why) ||
-        (desc->dtype == AXONN_BF16 && S.g[AX_Z] == 1 &&
-         !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why)))
+        (S.g[AX_Z] == 1 &&
+         !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why,
+                      static_cast<int>(elem_size(grad_dtype(desc->dtype))))))
       return cleanup(fail(AXONN_ERR_NCCL, "fused all-reduce buffers: %s", why.c_str()));
   }
-  if (desc->dtype == AXONN_BF16 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
+  if (desc->dtype != AXONN_F32 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
       geo.what_len % 8 == 0 && geo.m_l > 0) {
     std::string why;
     const int P = S.g[AX_Z];
     h->fz.axis = AX_Z;
+    h->fz.es = static_cast<int>(elem_size(grad_dtype(desc->dtype)));
     h->fz.elems = static_cast<size_t>(geo.k_l * geo.n_l);
-    if (!axonn::sym_alloc(&S.sym[AX_Z], h->fz.elems * 2, &h->fz.recv, &why) ||
+    if (!axonn::sym_alloc(&S.sym[AX_Z], h->fz.elems * h->fz.es, &h->fz.recv, &why) ||
         !axonn::sym_alloc(&S.sym[AX_Z], static_cast<size_t>(geo.what_len) * 2, &h->wstage, &why))
       return cleanup(fail(AXONN_ERR_NCCL, "fused Z buffers: %s", why.c_str()));
     h->fz.epi.mode = axonn::kScatter;
@@ -851,11 +857,12 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
       CUDA_TRY(cudaStreamWaitEvent(zs, h->ev_rs, 0));
       STATUS_TRY(fused_barrier(AX_Z, zs));  // every rank's scatter has landed
       CUDA_TRY(axonn::sym_owner_reduce(&h->fz.recv, nullptr, h->fz.epi.slice, h->fz.epi.P,
-                                       h->fz.epi.me, S.num_sms, zs, dW_hat));
+                                       h->fz.epi.me, S.num_sms, zs, dW_hat, nullptr,
+                                       h->fz.es == 4));
       g_launches.fetch_add(1);
       STATUS_TRY(fused_barrier(AX_Z, zs));  // every owner is done with its slots
       CUDA_TRY(record_xcall(h->ev_rsdone, zs));
-      count_comm(1, S.g[AX_Z], S_el, dt);
+      count_comm(1, S.g[AX_Z], S_el, gdt);
       CUDA_TRY(cudaEventRecord(h->ev_grad, zs));
       last = h->ev_grad;
     } else if (rs) {
@@ -908,7 +915,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     if (!fW) STATUS_TRY(grad_comm());
     STATUS_TRY(dI_gemm());
   }
-  if (fW) count_comm(4, S.g[AX_D], S_el, dt);
+  if (fW) count_comm(4, S.g[AX_D], S_el, gdt);
   // fused dI: every rank's reductions have landed after this
   if (fI) STATUS_TRY(fused_post(h->fi, st));
   if (fI && dI_local != h->fi.out.ptr)
@@ -923,7 +930,8 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     CUDA_TRY(cudaStreamWaitEvent(ds, h->ev_rs, 0));
     STATUS_TRY(fused_post(h->fw, ds, 1));
     if (dW_hat != h->fw.out.ptr)
-      CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fw.out.ptr, S_el * es, cudaMemcpyDeviceToDevice, ds));
+      CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fw.out.ptr, S_el * h->fw.es, cudaMemcpyDeviceToDevice,
+                               ds));
     CUDA_TRY(record_xcall(h->ev_wdone, ds));
     CUDA_TRY(cudaEventRecord(h->ev_grad, ds));
     last = h->ev_grad;

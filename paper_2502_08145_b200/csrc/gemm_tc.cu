@@ -612,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                 const int o = static_cast<int>(f / epi.slice);
                 const long long off =
                     static_cast<long long>(epi.me) * epi.slice + (f - o * epi.slice);
-                *reinterpret_cast<uint4*>(epi.peer[o] + static_cast<uint64_t>(off) * 2) = w;
+                *reinterpret_cast<uint4*>(epi.peer[o] + static_cast<uint64_t>(off) * ELEM) = w;
               } else if (vec_ok && gcol + UCOLS <= N) {
                 *reinterpret_cast<uint4*>(Cb + (static_cast<int64_t>(grow) * ldc + gcol) * ELEM) = w;
               } else if (OUTF) {
@@ -836,10 +836,12 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (!ok) return GemmStatus::kTensorMap;
   cudaError_t e;
   const EpiTarget epi = epi_in ? *epi_in : EpiTarget();
-  if (epi.mode != kStore && (single || (N & 7) || (ldc & 7) || out_f32))
+  const int unit = out_f32 ? 4 : 8;  // elements per 16-B epilogue unit
+  if (epi.mode != kStore && (single || (N % unit) || (ldc % unit)))
     return GemmStatus::kBadAlignment;
   if (out_f32 && op != 2) return GemmStatus::kBadOp;  // fp32 output: the dW (TN) product only
-  if (epi.mode == kScatter && (ldc != N || epi.slice % 8 || epi.P < 1 || epi.P > 8))
+  if (out_f32 && epi.mode == kMcRed) return GemmStatus::kBadAlignment;  // red.add is bf16 here
+  if (epi.mode == kScatter && (ldc != N || epi.slice % unit || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   // MT=2's single accumulator serialises the epilogue with the next tile; on
   // short K loops that costs more than its lower L2/DRAM traffic saves

@@ -63,6 +63,10 @@ __global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
 // received (fixed order src = 0..P-1, fp32, one RNE rounding to bf16) and
 // broadcast the result into every rank's output copy with multimem.st.  Every
 // element is reduced by exactly one rank, so all replicas hold the same bits.
+// F32 = false: 16-B units of 8 bf16, summed in fp32 in rank order and rounded
+// once (RNE); F32 = true: 4 fp32, summed in fp32 in rank order (fp32 gradient
+// reduction, reading R17).
+template <bool F32>
 __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, int P,
                                unsigned long long out_mc, uint4* __restrict__ out_local,
                                uint4* __restrict__ out_peer) {
@@ -75,15 +79,23 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, in
       const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        acc[2 * q] += __uint_as_float(w[q] << 16);
-        acc[2 * q + 1] += __uint_as_float(w[q] & 0xFFFF0000u);
+        if (F32) {
+          acc[q] += __uint_as_float(w[q]);
+        } else {
+          acc[2 * q] += __uint_as_float(w[q] << 16);
+          acc[2 * q + 1] += __uint_as_float(w[q] & 0xFFFF0000u);
+        }
       }
     }
     uint32_t o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
-      o[q] = *reinterpret_cast<uint32_t*>(&h);
+      if (F32) {
+        o[q] = __float_as_uint(acc[q]);
+      } else {
+        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+        o[q] = *reinterpret_cast<uint32_t*>(&h);
+      }
     }
     if (out_local) {  // reduce-scatter: the owner keeps its slice ...
       out_local[i] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -231,16 +243,18 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
 
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
                              int me, int num_sms, cudaStream_t st, void* out_local,
-                             void* out_peer) {
-  const long long n16 = slice / 8;
+                             void* out_peer, bool f32) {
+  const int es = f32 ? 4 : 2;
+  const long long n16 = slice * es / 16;
   long long blocks = (n16 + 255) / 256;
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
   if (blocks < 1) blocks = 1;
   const unsigned long long mc =
       out_local ? 0ULL
                 : reinterpret_cast<unsigned long long>(out->mc) +
-                      static_cast<unsigned long long>(me) * slice * 2;
-  k_owner_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+                      static_cast<unsigned long long>(me) * slice * es;
+  auto kern = f32 ? k_owner_reduce<true> : k_owner_reduce<false>;
+  kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
       reinterpret_cast<const uint4*>(recv->ptr), n16, P, mc, static_cast<uint4*>(out_local),
       static_cast<uint4*>(out_peer));
   return cudaGetLastError();

@@ -33,12 +33,13 @@ void sym_free(SymAxis* a, SymBuf* b);
 void* sym_peer_ptr(SymBuf* b, int peer);
 cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms);
 // Owner phase of the P-rank fused all-reduce / reduce-scatter (see sym.cu):
-// recv holds P slots of `slice` bf16 elements; the sum goes to every rank's
-// out[me*slice ...] (multicast), or to out_local when it is non-null (and also
-// to out_peer with plain NVLink stores when that is non-null: 2-rank axes).
+// recv holds P slots of `slice` elements (bf16, or fp32 when f32); the sum
+// goes to every rank's out[me*slice ...] (multicast), or to out_local when it
+// is non-null (and also to out_peer with plain NVLink stores when that is
+// non-null: 2-rank axes).
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
                              int me, int num_sms, cudaStream_t st, void* out_local = nullptr,
-                             void* out_peer = nullptr);
+                             void* out_peer = nullptr, bool f32 = false);
 // One-CTA cross-rank barrier on `st` (system-scope release/acquire).  Each
 // `index` (0 or 1) is its own barrier sequence: every rank must issue the
 // barriers of one index in the same order, and all barriers of one index must

@@ -282,10 +282,12 @@ def main():
                         run_case(cfg, m, k, n, transposed, "int", torch.float32, 1, rank, world)
                     results[(fused, m, k, n, transposed)] = run_case(
                         cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank, world)
-                    if fused == "red":
-                        # fp32 gradients: NCCL fp32 RS_z / AR_data beside fused bf16 AR_x/y
+                    if fused in ("red", "0"):
+                        # fp32 gradients: fused (scatter + fp32 owner phase) or NCCL fp32
+                        # RS_z / AR_data beside bf16 AR_x/y; integer dŴ bit-exact either way
                         run_case(cfg, m, k, n, transposed, "int", torch.bfloat16, 1, rank, world,
                                  grad_f32=True)
+                    if fused == "red":
                         zc = run_case(cfg, m, k, n, transposed, "uniform", torch.bfloat16, 1, rank,
                                       world, zero_copy=True)
                         if rank == 0:
