@@ -557,9 +557,9 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
       int cc[4] = {S.c[0], S.c[1], S.c[2], S.c[3]};
       cc[a] = 0;
       const int color = coords_to_rank(g, cc);
-      // Axis communicators run beside the persistent GEMM: their CTA budget is
-      // capped (AXONN_NCCL_MAX_CTAS, default 8) so they fit in the SMs the GEMM
-      // leaves free (axonn_set_gemm_sms).
+      // NCCL kernels (the paths not fused below) run beside the persistent GEMM:
+      // their CTA budget is capped (AXONN_NCCL_MAX_CTAS, default 8; 0 = NCCL's
+      // default) so they fit in SMs the GEMM leaves free (axonn_set_gemm_sms).
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
       const int max_ctas = env_int("AXONN_NCCL_MAX_CTAS", 8);
       if (max_ctas > 0) {
@@ -568,8 +568,8 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
         cfg.nvlsCTAs = max_ctas;
       }
       NCCL_TRY(ncclCommSplit(S.world_comm, color, S.c[a], &S.axis_comm[a], &cfg));
-      // Fused GEMM + all-reduce over NVLS for 2-rank axes (AXONN_FUSED=0 disables).
-      // With two ranks the switch computes RNE(a + b): bit-identical to NCCL.
+      // Symmetric memory for the fused GEMM + collective epilogues over NVLS
+      // (2..8 ranks of one NVSwitch domain; AXONN_FUSED=0 disables, §4.3).
       S.sym_why[a].clear();
       if (g[a] > 8)
         S.sym_why[a] = "fused all-reduce implemented for up to 8 ranks";
