@@ -557,11 +557,12 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
       int cc[4] = {S.c[0], S.c[1], S.c[2], S.c[3]};
       cc[a] = 0;
       const int color = coords_to_rank(g, cc);
-      // NCCL kernels (the paths not fused below) run beside the persistent GEMM:
-      // their CTA budget is capped (AXONN_NCCL_MAX_CTAS, default 8; 0 = NCCL's
-      // default) so they fit in SMs the GEMM leaves free (axonn_set_gemm_sms).
+      // NCCL kernels (the paths not fused below): NCCL's own CTA budget by
+      // default; AXONN_NCCL_MAX_CTAS=n caps it (to fit beside a GEMM given
+      // fewer SMs with axonn_set_gemm_sms).  Measured at G=4: capping at 8 costs
+      // 0.6% on (1,1,2,2) and 2% on the all-NCCL (1,1,1,4) step.
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-      const int max_ctas = env_int("AXONN_NCCL_MAX_CTAS", 8);
+      const int max_ctas = env_int("AXONN_NCCL_MAX_CTAS", 0);
       if (max_ctas > 0) {
         cfg.maxCTAs = max_ctas;
         cfg.minCTAs = std::min(max_ctas, env_int("AXONN_NCCL_MIN_CTAS", 1));
