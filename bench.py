@@ -269,6 +269,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--w-init", default="scaled", choices=["scaled", "uniform"],
                     help="weights U(+-sqrt(3/k)) (random init) or U(-1,1)")
+    ap.add_argument("--recompute", action="store_true",
+                    help="activation checkpointing (PAPER.md:722-723): each layer's forward re-runs "
+                         "before its backward; flops counted 8mkn as Narayanan et al.'s formula does")
     ap.add_argument("--no-chain", action="store_true",
                     help="independent per-layer inputs (default: proj->fc1->fc2 chained)")
     args = ap.parse_args()
@@ -364,6 +367,8 @@ def main():
             if i + 1 < len(L):  # OAG: prefetch the next layer's all-gather
                 ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], s)
         for l in reversed(L):
+            if args.recompute:  # checkpointing: Alg. 1 lines 1-7 again, then 9-15
+                ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
             ax.axonn_fc_backward(l["h"], l["dO"], l["dI"], l["dW"], s)
         ax.axonn_grads_sync(s)
 
@@ -423,7 +428,8 @@ def main():
     if graph is not None:  # events captured once hold the last replay: one step
         gemm_n, gemm_ms, gemm_flops = gemm_n * args.steps, gemm_ms * args.steps, gemm_flops * args.steps
     t_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
-    flops_step = model_flops(layers)              # whole job (all ranks)
+    # whole job (all ranks): 6mkn per layer, 8mkn with recomputation
+    flops_step = model_flops(layers) * (8.0 / 6.0 if args.recompute else 1.0)
     value = flops_step / (t_ms * 1e-3) / 1e12
 
     peaks, peaks_src = read_peaks()
@@ -499,6 +505,9 @@ def main():
                     if i in ext_dO:
                         stream.wait_event(evO[b][i])
                     stream.wait_event(ev_read[i])    # previous step's dŴ has reached the host
+                    if args.recompute:
+                        ax.axonn_fc_forward(L[i]["h"], dev_sets[b][i][0], L[i]["W"], L[i]["O"],
+                                            stream)
                     ax.axonn_fc_backward(L[i]["h"], dev_sets[b][i][1], L[i]["dI"], L[i]["dW"], stream)
                 ax.axonn_grads_sync(stream)
                 ev_free[b].record(stream)
@@ -562,6 +571,8 @@ def main():
             for l, (g, Wf, _) in zip(L, scratch):
                 ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, s)
             for l, (g, Wf, dWf) in zip(reversed(L), reversed(scratch)):
+                if args.recompute:
+                    ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, s)
                 ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, s)
                 ax.axonn_gemm(2, 0, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, s)
 
@@ -638,7 +649,8 @@ def main():
                      + ("U(+-sqrt(3/k)) random init" if args.w_init == "scaled" else "U(-1,1)")
                      + ", device-generated, seeded)"),
             "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu),
-                       "chained": chain},
+                       "chained": chain, "recompute": bool(args.recompute),
+                       "flops_per_layer": "8mkn (forward recomputed)" if args.recompute else "6mkn"},
             "per_gpu_tflops": value / world,
             "frac_of_peak": {"advertised_2250": value / world / 2250.0,
                              "measured_burst": value / world / burst,
