@@ -215,11 +215,12 @@ def run_reference(args):
     emit(out)
 
 
-def workload_config(model, n, grid, tpg=16384):
+def workload_config(model, n, grid, tpg=16384, blocks=1):
     h = HIDDEN[model]
-    return {"workload": (f"GPT-{model} block FC layers (QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h; "
+    return {"workload": ((f"{blocks} chained " if blocks > 1 else "") + f"GPT-{model} block FC layers (QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h; "
                          f"h={h}) Alg. 1 fwd+bwd, {tpg} tokens per GPU"
-                         + (" (BASELINE.json configs[1], C2)" if n == 1 and model == "5B" and tpg == 16384
+                         + (" (BASELINE.json configs[1], C2)"
+                            if n == 1 and model == "5B" and tpg == 16384 and blocks == 1
                             else f", global m={tpg * n}")),
             "grid": list(grid) if grid else [1, 1, 1, 1], "tokens": tpg * n, "hidden": h,
             "phase": "A (proj, fc2 transposed)",
@@ -269,6 +270,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--w-init", default="scaled", choices=["scaled", "uniform"],
                     help="weights U(+-sqrt(3/k)) (random init) or U(-1,1)")
+    ap.add_argument("--blocks", type=int, default=1,
+                    help="GPT blocks per step, chained fc2 -> next QKV (SURVEY.md §8(f) f-1)")
     ap.add_argument("--recompute", action="store_true",
                     help="activation checkpointing (PAPER.md:722-723): each layer's forward re-runs "
                          "before its backward; flops counted 8mkn as Narayanan et al.'s formula does")
@@ -299,7 +302,7 @@ def main():
 
     h = HIDDEN[args.model]
     m = args.tokens_per_gpu * world
-    layers = block_layers(h, m)
+    layers = block_layers(h, m) * args.blocks
     if args.grid:
         grid = tuple(int(x) for x in args.grid.split(","))
     elif world == 1:
@@ -345,7 +348,16 @@ def main():
                 rec[key] = ptr
         L.append(rec)
     # inputs: external (uniform(-1,1), uploaded by e2e) or chained
-    ext_I, ext_dO = ([0, 1], [3, 0]) if chain else (list(range(4)), list(reversed(range(4))))
+    # chained: inside a block proj -> fc1 -> fc2; across blocks fc2 (transposed,
+    # columns over Y) -> the next block's QKV (normal, input columns over Y).
+    # External: the first QKV input, every proj input (attention output), the
+    # last fc2's dO (loss gradient) and every QKV dO (attention backward).
+    nL = len(layers)
+    if chain:
+        ext_I = [i for i in range(nL) if i == 0 or i % 4 == 1]
+        ext_dO = [i for i in reversed(range(nL)) if i == nL - 1 or i % 4 == 0]
+    else:
+        ext_I, ext_dO = list(range(nL)), list(reversed(range(nL)))
     for i, l in enumerate(L):
         g = l["g"]
         if i in ext_I:
@@ -589,7 +601,8 @@ def main():
 
         # per layer: Alg. 1 forward / backward through the ABI vs the same
         # local products alone (SURVEY.md §8(d) "per layer and per block")
-        names = ["qkv", "proj", "fc1", "fc2"]
+        names = [["qkv", "proj", "fc1", "fc2"][i % 4] + (f"{i // 4}" if args.blocks > 1 else "")
+                 for i in range(nL)]
         nrep = max(3, min(args.steps, 20))
         ev = {key: [torch.cuda.Event(enable_timing=True) for _ in range(2 * nrep)]
               for key in [f"{n_}_{ph}" for n_ in names for ph in ("fwd", "bwd", "fwd_gemm", "bwd_gemm")]
@@ -648,7 +661,7 @@ def main():
             "data": ("synthetic (inputs uniform(-1,1) bf16, weights "
                      + ("U(+-sqrt(3/k)) random init" if args.w_init == "scaled" else "U(-1,1)")
                      + ", device-generated, seeded)"),
-            "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu),
+            "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu, args.blocks),
                        "chained": chain, "recompute": bool(args.recompute),
                        "flops_per_layer": "8mkn (forward recomputed)" if args.recompute else "6mkn"},
             "per_gpu_tflops": value / world,
