@@ -375,9 +375,11 @@ def main():
 
     def step(s):
         for i, l in enumerate(L):
-            ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
-            if i + 1 < len(L):  # OAG: prefetch the next layer's all-gather
+            # OAG: the next layer's all-gather is issued before
+            # this layer's forward, so it runs on the copy engines beside this GEMM
+            if i + 1 < len(L):
                 ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], s)
+            ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
         for l in reversed(L):
             if args.recompute:  # checkpointing: Alg. 1 lines 1-7 again, then 9-15
                 ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
@@ -508,11 +510,11 @@ def main():
             b = s_idx % 2
             with torch.cuda.stream(stream):
                 for i, l in enumerate(L):
+                    if i + 1 < len(L):
+                        ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
                     if i in ext_I:
                         stream.wait_event(evI[b][i])
                     ax.axonn_fc_forward(l["h"], dev_sets[b][i][0], l["W"], l["O"], stream)
-                    if i + 1 < len(L):
-                        ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
                 for i in reversed(range(len(L))):
                     if i in ext_dO:
                         stream.wait_event(evO[b][i])
@@ -611,11 +613,11 @@ def main():
         for rep in range(nrep):
             with torch.cuda.stream(stream):
                 for i, l in enumerate(L):
+                    if i + 1 < len(L):
+                        ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
                     ev[f"{names[i]}_fwd"][2 * rep].record(stream)
                     ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], stream)
                     ev[f"{names[i]}_fwd"][2 * rep + 1].record(stream)
-                    if i + 1 < len(L):
-                        ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
                 for i in reversed(range(len(L))):
                     l = L[i]
                     ev[f"{names[i]}_bwd"][2 * rep].record(stream)

@@ -162,8 +162,11 @@ axonn_status_t axonn_nvlink_probe(int axis, int64_t bytes, int mode, int ctas, i
                                   double* gbps);
 
 /* OAG: start the Z all-gather of W_hat for the NEXT
- * forward now, on the communication stream, after the work already enqueued
- * on `stream`.  Optional; axonn_fc_forward issues it itself if not prefetched. */
+ * forward of h now, on the communication stream (copy engines, no SMs), after
+ * the work already enqueued on `stream`.  To overlap it with layer i's GEMM,
+ * call prefetch(layer i+1) BEFORE forward(layer i).  Optional: a forward
+ * that was not prefetched gathers inline on `stream` with every SM pulling
+ * from the peers' staging copies (it would wait for the gather anyway). */
 axonn_status_t axonn_fc_prefetch(axonn_fc_t h, const void* W_hat, void* stream);
 
 /* Forward, Alg. 1 lines 1-7:

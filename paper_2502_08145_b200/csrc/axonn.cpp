@@ -429,6 +429,25 @@ axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
   return AXONN_OK;
 }
 
+// inline: a forward that was not prefetched needs W_{j,i} at once, so the
+// gather runs on the caller's stream itself with every SM pulling (Z barrier
+// sequence 1), independent of prefetches queued on the Z stream (sequence 0).
+// Staging reuse stays ordered across the two sequences: every gather's
+// completion is joined into the caller's stream before its forward GEMM.
+// Returns with h->prefetched = false and nothing to wait for.
+axonn_status_t gather_inline(axonn_fc* h, const void* W_hat, cudaStream_t st) {
+  const size_t bytes = static_cast<size_t>(h->geo.what_len) * elem_size(h->d.dtype);
+  STATUS_TRY(fused_barrier(AX_Z, st, 1));  // peers are done reading my previous staging
+  CUDA_TRY(cudaMemcpyAsync(h->wstage.ptr, W_hat, bytes, cudaMemcpyDeviceToDevice, st));
+  STATUS_TRY(fused_barrier(AX_Z, st, 1));  // every rank's Ŵ is staged
+  std::vector<const void*> src(S.g[AX_Z]);
+  for (int q = 0; q < S.g[AX_Z]; ++q) src[q] = q == S.c[AX_Z] ? W_hat : h->wpeer[q];
+  CUDA_TRY(axonn::sym_gather_pull(src.data(), S.g[AX_Z], bytes, h->wbuf, S.num_sms, st));
+  g_launches.fetch_add(1);
+  count_comm(0, S.g[AX_Z], static_cast<size_t>(h->geo.what_len), h->d.dtype);
+  return AXONN_OK;
+}
+
 axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) {
   if (S.g[AX_Z] == 1) {
     h->prefetched = true;
@@ -754,10 +773,17 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
   STATUS_TRY(check_async_nccl());
   cudaStream_t st = as_stream(stream);
   // line 2: W_{j,i} = all-gather_z(W_hat)
-  if (!h->prefetched) STATUS_TRY(issue_allgather(h, W_hat, st));
+  bool inline_ag = false;
+  if (!h->prefetched) {
+    inline_ag = S.g[AX_Z] > 1 && h->wstage.ptr && env_int("AXONN_AG_INLINE", 1) != 0;
+    if (inline_ag)
+      STATUS_TRY(gather_inline(h, W_hat, st));
+    else
+      STATUS_TRY(issue_allgather(h, W_hat, st));
+  }
   h->prefetched = false;
   const void* W = S.g[AX_Z] > 1 ? h->wbuf : W_hat;
-  if (S.g[AX_Z] > 1) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ag, 0));
+  if (S.g[AX_Z] > 1 && !inline_ag) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ag, 0));
   const int P = S.g[h->ax_fwd];
   const size_t es = elem_size(h->d.dtype);
   if (h->fo.epi.mode != axonn::kStore) {

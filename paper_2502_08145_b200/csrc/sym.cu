@@ -110,6 +110,23 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, in
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+// AG_z pull on the SMs: dst[q*n16 + i] = src[q][i] for the P ranks' staged
+// slices (LSA peer addresses; q == me is local).  Used when nothing runs
+// beside the gather (a forward that was not prefetched), where the copy
+// engines' serialised per-peer copies are slower than every SM pulling.
+struct PullSrc {
+  const uint4* p[8];
+};
+__global__ void k_gather_pull(PullSrc src, int P, long long n16, uint4* __restrict__ dst) {
+  const long long total = static_cast<long long>(P) * n16;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += stride) {
+    const int q = static_cast<int>(idx / n16);
+    dst[idx] = src.p[q][idx - q * n16];
+  }
+}
+
 __global__ void k_barrier(ncclDevComm dc, uint32_t index) {
   ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), index);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
@@ -257,6 +274,20 @@ cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long sl
   kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
       reinterpret_cast<const uint4*>(recv->ptr), n16, P, mc, static_cast<uint4*>(out_local),
       static_cast<uint4*>(out_peer));
+  return cudaGetLastError();
+}
+
+cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* dst, int num_sms,
+                            cudaStream_t st) {
+  if (P < 1 || P > 8 || bytes % 16) return cudaErrorInvalidValue;
+  PullSrc ps{};
+  for (int q = 0; q < P; ++q) ps.p[q] = static_cast<const uint4*>(src[q]);
+  const long long n16 = static_cast<long long>(bytes / 16);
+  long long blocks = (P * n16 + 255) / 256;
+  if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
+  if (blocks < 1) blocks = 1;
+  k_gather_pull<<<static_cast<unsigned>(blocks), 256, 0, st>>>(ps, P, n16,
+                                                               static_cast<uint4*>(dst));
   return cudaGetLastError();
 }
 

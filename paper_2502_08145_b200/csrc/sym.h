@@ -40,6 +40,10 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
 cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
                              int me, int num_sms, cudaStream_t st, void* out_local = nullptr,
                              void* out_peer = nullptr, bool f32 = false);
+// All-gather pull on the SMs: dst = src[0] | src[1] | ... | src[P-1], each
+// `bytes` long (bytes % 16 == 0; src are LSA peer addresses or local).
+cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* dst, int num_sms,
+                            cudaStream_t st);
 // One-CTA cross-rank barrier on `st` (system-scope release/acquire).  Each
 // `index` (0 or 1) is its own barrier sequence: every rank must issue the
 // barriers of one index in the same order, and all barriers of one index must

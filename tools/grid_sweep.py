@@ -89,9 +89,9 @@ def time_grid(cfg, layers, steps, warmup, chunks):
 
     def step():
         for i, l in enumerate(L):
-            ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
-            if i + 1 < len(L):
+            if i + 1 < len(L):  # OAG: next layer's gather beside this layer's GEMM
                 ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], s)
+            ax.axonn_fc_forward(l["h"], l["I"], l["W"], l["O"], s)
         for l in reversed(L):
             ax.axonn_fc_backward(l["h"], l["dO"], l["dI"], l["dW"], s)
         ax.axonn_grads_sync(s)
