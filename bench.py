@@ -54,6 +54,19 @@ def block_layers(h: int, m: int):
     return [(m, h, 3 * h, False), (m, h, h, True), (m, h, 4 * h, False), (m, 4 * h, h, True)]
 
 
+def chain_plan(n_layers: int, chain: bool = True):
+    """Which layers of a run of GPT blocks (4 FC layers each, phase A) take
+    external inputs.  Chained: layer i's I is layer i-1's O
+    and its dO is layer i+1's dI, except the first QKV input, every proj input
+    (attention output), the last fc2's dO (loss gradient) and every QKV dO
+    (attention backward).  Returns (ext_I ascending, ext_dO in backward order)."""
+    if not chain:
+        return list(range(n_layers)), list(reversed(range(n_layers)))
+    ext_I = [i for i in range(n_layers) if i == 0 or i % 4 == 1]
+    ext_dO = [i for i in reversed(range(n_layers)) if i == n_layers - 1 or i % 4 == 0]
+    return ext_I, ext_dO
+
+
 def model_flops(layers) -> float:
     return float(sum(6 * m * k * n for m, k, n, _ in layers))
 
@@ -353,11 +366,7 @@ def main():
     # External: the first QKV input, every proj input (attention output), the
     # last fc2's dO (loss gradient) and every QKV dO (attention backward).
     nL = len(layers)
-    if chain:
-        ext_I = [i for i in range(nL) if i == 0 or i % 4 == 1]
-        ext_dO = [i for i in reversed(range(nL)) if i == nL - 1 or i % 4 == 0]
-    else:
-        ext_I, ext_dO = list(range(nL)), list(reversed(range(nL)))
+    ext_I, ext_dO = chain_plan(nL, chain)
     for i, l in enumerate(L):
         g = l["g"]
         if i in ext_I:

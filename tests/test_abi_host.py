@@ -110,3 +110,31 @@ def test_grid_select_errors():
     with pytest.raises(ax.AxonnError) as e:
         ax.axonn_grid_select([(64, 64, 64, False)], 4, 8, {}, 1e9)
     assert e.value.status == ax.AXONN_ERR_CONFIG and "G0=1, G1=" in str(e.value)
+
+
+def test_chain_plan_and_layouts_on_every_grid():
+    """The chained block bench.py times: every non-external
+    input is the previous layer's output shard, byte for byte, on every grid of
+    up to 16 ranks — checked through the ABI's host geometry."""
+    from bench import block_layers, chain_plan
+    assert chain_plan(4) == ([0, 1], [3, 0])
+    assert chain_plan(8) == ([0, 1, 5], [7, 4, 0])
+    assert chain_plan(4, chain=False) == ([0, 1, 2, 3], [3, 2, 1, 0])
+    layers = block_layers(64, 256) * 2          # two blocks, h = 64, m = 256
+    ext_I, ext_dO = chain_plan(len(layers))
+    checked = 0
+    for G in (1, 2, 4, 8, 16):
+        for cfg in grid.enumerate_configs(G):
+            if not all(pm.feasible(pm.Layer(*L), cfg) for L in layers):
+                continue
+            for r in range(G):
+                geo = [ax.axonn_shard_geometry(m, k, n, cfg, r, t) for (m, k, n, t) in layers]
+                for i in range(len(layers)):
+                    if i not in ext_I:      # I_i == O_{i-1}: same rows, same columns
+                        p, g = geo[i - 1], geo[i]
+                        assert (p.m_l, p.row0, p.n_l, p.out_col0) == (g.m_l, g.row0, g.k_l, g.in_col0)
+                    if i not in ext_dO:     # dO_i == dI_{i+1}
+                        q, g = geo[i + 1], geo[i]
+                        assert (q.m_l, q.row0, q.k_l, q.in_col0) == (g.m_l, g.row0, g.n_l, g.out_col0)
+            checked += 1
+    assert checked > 30
