@@ -285,6 +285,8 @@ def main():
                     help="weights U(+-sqrt(3/k)) (random init) or U(-1,1)")
     ap.add_argument("--blocks", type=int, default=1,
                     help="GPT blocks per step, chained fc2 -> next QKV (SURVEY.md §8(f) f-1)")
+    ap.add_argument("--grad-f32", action="store_true",
+                    help="AXONN_BF16_GRADF32: dW in fp32, RS_z / data-parallel sums in fp32 (R17)")
     ap.add_argument("--recompute", action="store_true",
                     help="activation checkpointing (PAPER.md:722-723): each layer's forward re-runs "
                          "before its backward; flops counted 8mkn as Narayanan et al.'s formula does")
@@ -342,9 +344,14 @@ def main():
         return t.to(bf)
 
     chain = not args.no_chain
+    gdt = torch.float32 if args.grad_f32 else bf   # dŴ storage
+    gsz = 4 if args.grad_f32 else 2
+    gcode = ax.AXONN_BF16_GRADF32 if args.grad_f32 else ax.AXONN_BF16  # dW product dtype
     L = []
     for (mm, k, n, t) in layers:
-        hd = ax.axonn_fc_create(mm, k, n, t, ax.AXONN_BF16, args.chunks)
+        hd = ax.axonn_fc_create(mm, k, n, t,
+                                ax.AXONN_BF16_GRADF32 if args.grad_f32 else ax.AXONN_BF16,
+                                args.chunks)
         g = ax.axonn_fc_geometry(hd)
         # random-init weights, variance preserving (U(+-sqrt(3/k)): unit-variance
         # outputs for unit-variance inputs), so chained activations stay O(1)
@@ -352,7 +359,7 @@ def main():
         rec = {"h": hd, "g": g, "W": rnd(g.what_len, scale=wscale),
                "O": torch.empty(g.m_l, g.n_l, dtype=bf, device="cuda"),
                "dI": torch.empty(g.m_l, g.k_l, dtype=bf, device="cuda"),
-               "dW": torch.empty(g.what_len, dtype=bf, device="cuda")}
+               "dW": torch.empty(g.what_len, dtype=gdt, device="cuda")}
         # outputs of fused (NVLS) all-reduces live in handle-owned symmetric
         # buffers; writing there avoids the final copy (include/axonn.h)
         for key, which in (("O", 0), ("dI", 1), ("dW", 2)):
@@ -487,7 +494,7 @@ def main():
             S_ = l["g"].what_len
             lo, hi = S_ * dcoord // gd, S_ * (dcoord + 1) // gd
             wsl.append((lo, hi))
-        hdW = [torch.empty(hi - lo, dtype=bf).pin_memory() for lo, hi in wsl]
+        hdW = [torch.empty(hi - lo, dtype=gdt).pin_memory() for lo, hi in wsl]
         dev_sets = [[(l["I"], l["dO"]) for l in L],
                     [(torch.empty_like(L[i]["I"]) if i in ext_I else L[i]["I"],
                       torch.empty_like(L[i]["dO"]) if i in ext_dO else L[i]["dO"])
@@ -499,9 +506,9 @@ def main():
         ev_done = torch.cuda.Event()
         ev_read = [torch.cuda.Event() for _ in L]
         bi = sum(t.numel() * 2 for t in list(hI.values()) + list(hdO.values()))
-        bo = sum(t.numel() * 2 for t in hdW)
+        bo = sum(t.numel() * gsz for t in hdW)
         # whole job: the slices' union is every weight-gradient element once
-        bo_total = sum(2 * k * n for (_, k, n, _) in layers)
+        bo_total = sum(gsz * k * n for (_, k, n, _) in layers)
         assert world > 1 or bo == bo_total
 
         def upload(s_idx):
@@ -540,7 +547,8 @@ def main():
                 for i in reversed(range(len(L))):    # in the next step's backward order
                     l = L[i]
                     if isinstance(l["dW"], int):
-                        copy_raw(hdW[i].data_ptr(), l["dW"] + 2 * wsl[i][0], hdW[i].numel() * 2, down)
+                        copy_raw(hdW[i].data_ptr(), l["dW"] + gsz * wsl[i][0], hdW[i].numel() * gsz,
+                                 down)
                     else:
                         hdW[i].copy_(l["dW"][wsl[i][0]:wsl[i][1]], non_blocking=True)
                     ev_read[i].record(down)
@@ -588,7 +596,7 @@ def main():
             g = l["g"]
             a = (3.0 / k_glob) ** 0.5 if args.w_init == "scaled" else 1.0  # as the Alg. 1 step
             scratch.append((g, torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda").uniform_(-a, a),
-                            torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda")))
+                            torch.empty(g.k_l, g.n_l, dtype=gdt, device="cuda")))
 
         def gemm_step(s):
             for l, (g, Wf, _) in zip(L, scratch):
@@ -597,7 +605,7 @@ def main():
                 if args.recompute:
                     ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, s)
                 ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, s)
-                ax.axonn_gemm(2, 0, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, s)
+                ax.axonn_gemm(2, gcode, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, s)
 
         for _ in range(2):
             gemm_step(stream)
@@ -641,7 +649,7 @@ def main():
                     ev[f"{names[i]}_fwd_gemm"][2 * rep + 1].record(stream)
                     ev[f"{names[i]}_bwd_gemm"][2 * rep].record(stream)
                     ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, stream)
-                    ax.axonn_gemm(2, 0, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, stream)
+                    ax.axonn_gemm(2, gcode, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, stream)
                     ev[f"{names[i]}_bwd_gemm"][2 * rep + 1].record(stream)
         barrier()
         for key, lst in ev.items():
@@ -674,6 +682,7 @@ def main():
                      + ", device-generated, seeded)"),
             "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu, args.blocks),
                        "chained": chain, "recompute": bool(args.recompute),
+                       "grad_f32": bool(args.grad_f32),
                        "flops_per_layer": "8mkn (forward recomputed)" if args.recompute else "6mkn"},
             "per_gpu_tflops": value / world,
             "frac_of_peak": {"advertised_2250": value / world / 2250.0,
