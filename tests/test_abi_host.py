@@ -138,3 +138,43 @@ def test_chain_plan_and_layouts_on_every_grid():
                         assert (q.m_l, q.row0, q.k_l, q.in_col0) == (g.m_l, g.row0, g.n_l, g.out_col0)
             checked += 1
     assert checked > 30
+
+
+def test_argument_and_state_errors_without_a_device():
+    """Calls that must fail before touching a GPU: the documented error kinds
+    (include/axonn.h) come back with a message, on a host with no device."""
+    def status(fn, *a):
+        with pytest.raises(ax.AxonnError) as e:
+            fn(*a)
+        assert str(e.value)           # every failure carries a message
+        return e.value.status
+
+    # grid arguments: a zero factor is a configuration error
+    assert status(ax.axonn_rank_to_coords, 0, (0, 1, 1, 1)) == ax.AXONN_ERR_CONFIG
+    assert status(ax.axonn_rank_to_coords, 5, (2, 1, 1, 2)) == ax.AXONN_ERR_ARG
+    try:
+        ax.axonn_grid_coords()
+        have_grid = True          # a GPU module in this process created one
+    except ax.AxonnError:
+        have_grid = False
+    if not have_grid:
+        # no grid yet: a layer handle is a state error
+        assert status(ax.axonn_fc_create, 64, 64, 64) == ax.AXONN_ERR_STATE
+        assert status(ax.axonn_grid_coords) == ax.AXONN_ERR_STATE
+        # a multi-rank grid needs bootstrap first
+        assert status(ax.axonn_grid_init, 2, 1, 1, 1) == ax.AXONN_ERR_STATE
+    # local-product argument checks precede any device access (stream 0: no torch CUDA)
+    g = lambda *a: ax.axonn_gemm(*a, 0)  # noqa: E731
+    assert status(g, 3, ax.AXONN_BF16, 8, 8, 8, 0, 8, 0, 8, 0, 8) == ax.AXONN_ERR_ARG
+    assert status(g, 0, 7, 8, 8, 8, 0, 8, 0, 8, 0, 8) == ax.AXONN_ERR_ARG
+    assert status(g, 0, ax.AXONN_BF16, -1, 8, 8, 0, 8, 0, 8, 0, 8) == ax.AXONN_ERR_ARG
+    assert status(g, 0, ax.AXONN_BF16, 8, 8, 8, 0, 8, 0, 8, 0, 8) == ax.AXONN_ERR_ARG
+    assert status(g, 0, ax.AXONN_BF16, 8, 16, 8, 1 << 20, 8, 1 << 20, 8, 1 << 20, 16) \
+        == ax.AXONN_ERR_ARG           # ldb < N
+    # geometry: bad dtype, negative sizes
+    assert status(ax.axonn_shard_geometry, 64, 64, 64, (1, 1, 1, 1), 0, False, 9) == ax.AXONN_ERR_ARG
+    assert status(ax.axonn_shard_geometry, -1, 64, 64, (1, 1, 1, 1), 0) == ax.AXONN_ERR_ARG
+    assert status(ax.axonn_shard_geometry, 64, 64, 64, (2, 1, 1, 1), 2) == ax.AXONN_ERR_ARG
+    # the grid-select mixed-precision entry validates its byte sizes
+    assert status(ax.axonn_grid_select_mp, [(64, 64, 64, False)], 2, 8,
+                  pm.uniform_table(8, 1e9), 1e9, 2, 0) == ax.AXONN_ERR_ARG
