@@ -192,6 +192,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import numpy  # noqa: F401  (load BLAS before lifting its thread limit)
+    try:
+        # torchrun exports OMP_NUM_THREADS=1 to every rank; this rank alone
+        # works, so the oracle gets every host core it may run on
+        from threadpoolctl import threadpool_limits
+        _blas = threadpool_limits(limits=len(os.sched_getaffinity(0)))  # noqa: F841
+    except Exception:  # pragma: no cover
+        pass
     n = args.gpus
     h = HIDDEN[args.model]
     m_ref = 256
