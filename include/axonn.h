@@ -5,7 +5,7 @@
  * Gx x Gy x Gz grid nested in Gd-way data parallelism.
  *
  * Citations "PAPER.md:N" are lines of the paper's LaTeX source; "Alg. 1" is
- * Algorithm 1.  DESIGN.md lists every reading (R1..R16)
+ * Algorithm 1.  DESIGN.md lists every reading (R1..R17)
  * taken where the paper is silent or ambiguous.
  *
  * Conventions for every call
@@ -17,6 +17,12 @@
  *     cudaStream_t passed as void*; NULL = legacy default stream): they
  *     enqueue work and return without synchronising.  Asynchronous CUDA /
  *     NCCL failures surface as AXONN_ERR_CUDA / AXONN_ERR_NCCL on a later call.
+ *   - Collective calls (forward, backward, prefetch, grads_sync) must be issued
+ *     in the same order on every rank, on one stream per rank (or on streams
+ *     the caller orders): their cross-rank barriers are per-axis sequences
+ *     that must not run concurrently.  The library's own side streams (one
+ *     per axis) are ordered internally.  CUDA-graph capture of such a
+ *     sequence is supported (external event nodes order it across replays).
  *   - All matrices are row-major with an explicit leading dimension in
  *     elements; bf16 buffers hold IEEE bfloat16, f32 buffers IEEE binary32.
  *   - No call ever falls back to a CPU path: if the CUDA device or the
