@@ -91,6 +91,7 @@ struct State {
   cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
   axonn::SymAxis sym[4];          // NVLS symmetric memory per axis (fused all-reduce)
   std::string sym_why[4];         // why an axis has no fused path
+  int* flag_dev = nullptr;        // agree_all scratch
   std::vector<cudaEvent_t> pending_grads;
   std::set<struct ::axonn_fc*> handles;
   bool profiling = false;
@@ -334,6 +335,7 @@ struct axonn_fc {
   Fused fz;   // RS_z fused into line 13: the epilogue scatters to the slice owners
   axonn::SymBuf wstage;        // AG_z over copy engines: symmetric staging copy of Ŵ
   std::vector<void*> wpeer;    // every Z rank's staging address (LSA)
+  std::string fused_why;            // non-empty: fused buffers fell back to NCCL
   cudaEvent_t ev_rsdone = nullptr;  // last fused RS_z finished reading its slots
   cudaEvent_t ev_wdone = nullptr;   // last deferred data-parallel reduction finished
 };
@@ -405,6 +407,29 @@ bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64
 }
 
 axonn_status_t fused_barrier(int axis, cudaStream_t st, int index = 0);
+
+// Back to the NCCL path: free a fused record's windows and clear its target.
+void fused_reset(axonn_fc::Fused* f) {
+  axonn::sym_free(&S.sym[f->axis], &f->out);
+  axonn::sym_free(&S.sym[f->axis], &f->recv);
+  f->epi = axonn::EpiTarget();
+  f->out_peer = nullptr;
+  f->elems = 0;
+}
+
+// *ok := AND over every rank of the world (host; synchronous; no-op at 1 rank).
+axonn_status_t agree_all(bool* ok) {
+  if (S.world <= 1 || !S.world_comm) return AXONN_OK;
+  if (!S.flag_dev) CUDA_TRY(cudaMalloc(&S.flag_dev, sizeof(int)));
+  int v = *ok ? 1 : 0;
+  cudaStream_t st = S.cstream[AX_X];  // the library's own stream, never under capture
+  CUDA_TRY(cudaMemcpyAsync(S.flag_dev, &v, sizeof v, cudaMemcpyHostToDevice, st));
+  NCCL_TRY(ncclAllReduce(S.flag_dev, S.flag_dev, 1, ncclInt32, ncclMin, S.world_comm, st));
+  CUDA_TRY(cudaMemcpyAsync(&v, S.flag_dev, sizeof v, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *ok = v != 0;
+  return AXONN_OK;
+}
 
 axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
   if (f.epi.mode == axonn::kMcRed) {
@@ -632,6 +657,8 @@ axonn_status_t axonn_grid_finalize(void) {
     S.cstream[a] = nullptr;
   }
   S.pending_grads.clear();
+  if (S.flag_dev) cudaFree(S.flag_dev);
+  S.flag_dev = nullptr;
   S.grid = false;
   return AXONN_OK;
 }
@@ -674,37 +701,53 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
                          &h->ev_rsdone, &h->ev_wdone})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
+  // Fused (NVLS) buffers.  A failure here is not fatal: the layer falls back
+  // to NCCL collectives (still the GPU path), but only if EVERY rank does, so
+  // the ranks agree (MIN over the world) before anything is used.
+  std::string why;
+  bool ok = true;
   if (desc->dtype != AXONN_F32) {
     // O and dI reduce bf16; dŴ in its gradient precision (fp32 for AXONN_BF16_GRADF32)
-    std::string why;
-    if (!fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, &why) ||
-        !fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, &why) ||
-        (S.g[AX_Z] == 1 &&
-         !fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why,
-                      static_cast<int>(elem_size(grad_dtype(desc->dtype))))))
-      return cleanup(fail(AXONN_ERR_NCCL, "fused all-reduce buffers: %s", why.c_str()));
+    ok = fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, &why) &&
+         fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, &why) &&
+         (S.g[AX_Z] > 1 ||
+          fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why,
+                      static_cast<int>(elem_size(grad_dtype(desc->dtype)))));
   }
-  if (desc->dtype != AXONN_F32 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
+  if (ok && desc->dtype != AXONN_F32 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
       geo.what_len % 8 == 0 && geo.m_l > 0) {
-    std::string why;
     const int P = S.g[AX_Z];
     h->fz.axis = AX_Z;
     h->fz.es = static_cast<int>(elem_size(grad_dtype(desc->dtype)));
     h->fz.elems = static_cast<size_t>(geo.k_l * geo.n_l);
-    if (!axonn::sym_alloc(&S.sym[AX_Z], h->fz.elems * h->fz.es, &h->fz.recv, &why) ||
-        !axonn::sym_alloc(&S.sym[AX_Z], static_cast<size_t>(geo.what_len) * 2, &h->wstage, &why))
-      return cleanup(fail(AXONN_ERR_NCCL, "fused Z buffers: %s", why.c_str()));
-    h->fz.epi.mode = axonn::kScatter;
-    h->fz.epi.P = P;
-    h->fz.epi.me = S.c[AX_Z];
-    h->fz.epi.slice = geo.what_len;  // owner of flat index f is f / S = its Ŵ slice (R4)
-    h->wpeer.resize(P);
-    for (int q = 0; q < P; ++q) {
-      h->fz.epi.peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&h->fz.recv, q));
-      h->wpeer[q] = axonn::sym_peer_ptr(&h->wstage, q);
-      if (!h->fz.epi.peer[q] || !h->wpeer[q])
-        return cleanup(fail(AXONN_ERR_NCCL, "peer address of a Z window unavailable"));
+    ok = axonn::sym_alloc(&S.sym[AX_Z], h->fz.elems * h->fz.es, &h->fz.recv, &why) &&
+         axonn::sym_alloc(&S.sym[AX_Z], static_cast<size_t>(geo.what_len) * 2, &h->wstage, &why);
+    if (ok) {
+      h->fz.epi.mode = axonn::kScatter;
+      h->fz.epi.P = P;
+      h->fz.epi.me = S.c[AX_Z];
+      h->fz.epi.slice = geo.what_len;  // owner of flat index f is f / S = its Ŵ slice (R4)
+      h->wpeer.resize(P);
+      for (int q = 0; q < P && ok; ++q) {
+        h->fz.epi.peer[q] =
+            reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&h->fz.recv, q));
+        h->wpeer[q] = axonn::sym_peer_ptr(&h->wstage, q);
+        if (!h->fz.epi.peer[q] || !h->wpeer[q]) {
+          why = "peer address of a Z window unavailable";
+          ok = false;
+        }
+      }
     }
+  }
+  bool all_ok = ok;
+  STATUS_TRY(agree_all(&all_ok));
+  if (!all_ok) {
+    for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz}) fused_reset(f);
+    axonn::sym_free(&S.sym[AX_Z], &h->wstage);
+    h->wpeer.clear();
+    h->fused_why = ok ? "another rank could not allocate its fused buffers" : why;
+    std::fprintf(stderr, "[axonn] rank %d: fused NVLS buffers unavailable (%s); this layer uses "
+                 "NCCL collectives\n", S.rank, h->fused_why.c_str());
   }
   h->ev_chunk.resize(h->d.chunks + 1, nullptr);
   for (auto& e : h->ev_chunk)

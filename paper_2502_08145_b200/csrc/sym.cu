@@ -17,6 +17,7 @@
 #include <nccl_device.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -175,6 +176,14 @@ bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why) {
   *out = SymBuf();
   if (!a->impl) {
     *why = "axis has no symmetric-memory communicator";
+    return false;
+  }
+  static const bool fail_test = [] {  // test hook: exercise the NCCL fallback
+    const char* v = std::getenv("AXONN_SYM_ALLOC_FAIL");
+    return v && std::atoi(v) != 0;
+  }();
+  if (fail_test) {
+    *why = "AXONN_SYM_ALLOC_FAIL set";
     return false;
   }
   bytes = (bytes + (2u << 20) - 1) & ~static_cast<size_t>((2u << 20) - 1);
