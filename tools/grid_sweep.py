@@ -116,11 +116,53 @@ def time_grid(cfg, layers, steps, warmup, chunks):
     return float(ms.item())
 
 
-def spearman(a, b):
+def tie_ranks(v, rel=1e-12):
+    """Average ranks (1-based), values equal within `rel` (R12's tolerance) tied."""
     import numpy as np
-    ra = np.argsort(np.argsort(a))
-    rb = np.argsort(np.argsort(b))
+    v = np.asarray(v, dtype=np.float64)
+    order = np.argsort(v, kind="stable")
+    ranks = np.empty(len(v))
+    i = 0
+    while i < len(v):
+        j = i
+        while j + 1 < len(v) and abs(v[order[j + 1]] - v[order[i]]) <= rel * max(abs(v[order[i]]), 1e-300):
+            j += 1
+        ranks[order[i:j + 1]] = (i + j) / 2.0 + 1.0
+        i = j + 1
+    return ranks
+
+
+def spearman(a, b):
+    """Spearman's rho with average ranks for ties (the model's exact Z-vs-DP
+    ties, R12, are not ordered arbitrarily)."""
+    import numpy as np
+    ra, rb = tie_ranks(a), tie_ranks(b)
+    if np.std(ra) == 0 or np.std(rb) == 0:
+        return float("nan")
     return float(np.corrcoef(ra, rb)[0, 1])
+
+
+def kendall_tau_b(a, b, rel=1e-12):
+    """Kendall's tau-b (tie-corrected) between predicted and measured orders."""
+    import math
+    n = len(a)
+    conc = disc = ta = tb = 0
+    for i in range(n):
+        for j in range(i + 1, n):
+            da = 0 if abs(a[i] - a[j]) <= rel * max(abs(a[i]), abs(a[j]), 1e-300) else (1 if a[i] > a[j] else -1)
+            db = 0 if abs(b[i] - b[j]) <= rel * max(abs(b[i]), abs(b[j]), 1e-300) else (1 if b[i] > b[j] else -1)
+            if da == 0 and db == 0:
+                continue
+            if da == 0:
+                ta += 1
+            elif db == 0:
+                tb += 1
+            elif da == db:
+                conc += 1
+            else:
+                disc += 1
+    den = math.sqrt((conc + disc + ta) * (conc + disc + tb))
+    return (conc - disc) / den if den else float("nan")
 
 
 def main():
@@ -168,6 +210,8 @@ def main():
                           "model_t_comm_uniform": u, "model_t_comm_measured_beta": p}
                          for c, u, p in zip(cfgs, pu, pm)],
                "spearman_uniform": spearman(pu, t), "spearman_measured_beta": spearman(pm, t),
+               "kendall_tau_b_uniform": kendall_tau_b(pu, t),
+               "kendall_tau_b_measured_beta": kendall_tau_b(pm, t),
                f"top{k}_hits_uniform": len(top_u & fastest),
                f"top{k}_hits_measured_beta": len(top_m & fastest)}
         s = json.dumps(out, indent=1)
