@@ -178,3 +178,49 @@ def test_argument_and_state_errors_without_a_device():
     # the grid-select mixed-precision entry validates its byte sizes
     assert status(ax.axonn_grid_select_mp, [(64, 64, 64, False)], 2, 8,
                   pm.uniform_table(8, 1e9), 1e9, 2, 0) == ax.AXONN_ERR_ARG
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/axonn.h is a C ABI: a C99 program compiles against it with
+    -Wall -Werror, links to libaxonn.so, and calls pure-host entry points
+    (version, rank <-> coordinates, shard geometry, grid_select) — no torch,
+    no C++."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2502_08145_b200")
+    src = tmp_path / "t.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "axonn.h"
+int main(void) {
+  int c[4];
+  axonn_fc_desc_t d = {4096, 1024, 512, 1, AXONN_BF16, 1};
+  axonn_geometry_t g;
+  axonn_layer_t L = {16384, 4096, 4096, 0};
+  axonn_bw_entry_t tb = {1, 2, 1e11};
+  axonn_grid_score_t out[4];
+  int n = 0;
+  if (axonn_version() <= 0) return 1;
+  if (axonn_rank_to_coords(13, 2, 2, 2, 2, c) != AXONN_OK) return 2;
+  if (c[0] != 1 || c[1] != 0 || c[2] != 1 || c[3] != 1) return 3;
+  if (axonn_shard_geometry(&d, 2, 2, 1, 1, 3, &g) != AXONN_OK) return 4;
+  if (axonn_grid_select(&L, 1, 2, 8, &tb, 1, 1e11, 2, 0, out, 4, &n) != AXONN_OK || n != 4) return 5;
+  if (axonn_gemm(9, AXONN_BF16, 8, 8, 8, 0, 8, 0, 8, 0, 8, 0) != AXONN_ERR_ARG) return 6;
+  printf("ok %d %lld %lld %d%d%d%d\n", axonn_version(), (long long)g.k_l, (long long)g.n_l,
+         out[0].gx, out[0].gy, out[0].gz, out[0].gd);
+  return 0;
+}
+''')
+    exe = tmp_path / "t"
+    cc = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I",
+                         os.path.join(root, "include"), str(src), "-L", libdir, "-laxonn",
+                         f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert run.returncode == 0 and run.stdout.startswith("ok"), (run.returncode, run.stdout, run.stderr)
+    # transposed layer on (2,2,1,1): k_l = k/Gx, n_l = n/Gy (R2)
+    assert run.stdout.split()[2:4] == ["512", "256"]
