@@ -49,9 +49,13 @@ HIDDEN = {"5B": 4096, "10B": 5120, "20B": 7168, "40B": 9216, "80B": 12288}
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
 
 
-def block_layers(h: int, m: int):
-    """(m, k, n, transposed) of the four FC layers of one GPT block, phase A (R2b)."""
-    return [(m, h, 3 * h, False), (m, h, h, True), (m, h, 4 * h, False), (m, 4 * h, h, True)]
+def block_layers(h: int, m: int, phase: str = "A"):
+    """(m, k, n, transposed) of the four FC layers of one GPT block (Table II
+    shapes).  Phase A transposes proj and fc2, phase B QKV and fc1 (R2b)."""
+    if phase not in ("A", "B"):
+        raise ValueError(f"phase must be 'A' or 'B', got {phase!r}")
+    t = [False, True, False, True] if phase == "A" else [True, False, True, False]
+    return [(m, h, 3 * h, t[0]), (m, h, h, t[1]), (m, h, 4 * h, t[2]), (m, 4 * h, h, t[3])]
 
 
 def chain_plan(n_layers: int, chain: bool = True):
@@ -188,7 +192,8 @@ def oracle_sample(h: int, m_sample: int, min_seconds: float):
 
 
 def run_reference(args):
-    """--impl reference: the oracle as it stands, on the host cores, rank 0 only."""
+    """--impl reference: the oracle as it stands, on the host cores, rank 0 only,
+    on a bounded sample of the primary workload of this GPU count."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -201,14 +206,21 @@ def run_reference(args):
     except Exception:  # pragma: no cover
         pass
     n = args.gpus
-    h = HIDDEN[args.model]
+    spec = PRIMARY.get(n) if not (args.model or args.grid or args.tokens or args.tokens_per_gpu) else None
+    if spec is None:
+        model = args.model or "5B"
+        spec = dict(model=model, m=args.tokens or (args.tokens_per_gpu or 16384) * n,
+                    grid=tuple(int(x) for x in args.grid.split(",")) if args.grid else None,
+                    phase=args.phase or "A", label="custom")
+    h = HIDDEN[spec["model"]]
     m_ref = 256
     import numpy as np
     from oracle import fc
     import synthdata
-    layers = block_layers(h, m_ref)
+    layers = block_layers(h, m_ref, spec.get("phase", "A"))
     data = [tuple(a.astype(np.float64) for a in synthdata.layer_tensors(m, k, nn, i))
             for i, (m, k, nn, _) in enumerate(layers)]
+
     def step():
         for X, W, dY in data:
             fc.fc_layer(X, W, dY)
@@ -224,28 +236,32 @@ def run_reference(args):
         threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
     except Exception:  # pragma: no cover
         threads = os.cpu_count()
-    sample = (f"oracle.fc fp64 on the GPT-{args.model} block's 4 FC layers fwd+bwd, {m_ref} token "
-              f"rows per step (bounded sample of the {16384 * n}-token workload)")
+    sample = (f"oracle.fc fp64 on the GPT-{spec['model']} block's 4 FC layers fwd+bwd, {m_ref} token "
+              f"rows per step (bounded sample of the {spec['m']}-token workload)")
     out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": n,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": workload_config(args.model, n, None),
+           "data": "synthetic",
+           "config": {**workload_config(spec["model"], n, spec.get("grid"), spec["m"], 1,
+                                        spec.get("phase", "A")), "label": spec.get("label", "")},
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
 
 
-def workload_config(model, n, grid, tpg=16384, blocks=1):
+def workload_config(model, n, grid, m, blocks=1, phase="A"):
+    """config of the JSON line: the workload named by BASELINE.json."""
     h = HIDDEN[model]
-    return {"workload": ((f"{blocks} chained " if blocks > 1 else "") + f"GPT-{model} block FC layers (QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h; "
-                         f"h={h}) Alg. 1 fwd+bwd, {tpg} tokens per GPU"
-                         + (" (BASELINE.json configs[1], C2)"
-                            if n == 1 and model == "5B" and tpg == 16384 and blocks == 1
-                            else f", global m={tpg * n}")),
-            "grid": list(grid) if grid else [1, 1, 1, 1], "tokens": tpg * n, "hidden": h,
-            "phase": "A (proj, fc2 transposed)",
-            "l2": "no flush: per-step operands (>= 134 MB each for I/dO of the fc2 layer) exceed the 126 MB L2"}
+    c2 = n == 1 and model == "5B" and m == 16384 and blocks == 1 and tuple(grid or (1, 1, 1, 1)) == (1, 1, 1, 1)
+    return {"workload": ((f"{blocks} chained " if blocks > 1 else "")
+                         + f"GPT-{model} block FC layers (QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h; "
+                         f"h={h}) Alg. 1 fwd+bwd, m={m} global tokens on {n} GPU(s)"
+                         + (" (BASELINE.json configs[1], C2)" if c2 else "")),
+            "grid": list(grid) if grid else [1, 1, 1, 1], "tokens": m, "hidden": h,
+            "phase": "A (proj, fc2 transposed)" if phase == "A" else "B (QKV, fc1 transposed)",
+            "l2": "no flush: per-step operands (>= 58 MB each, most >= 134 MB) exceed the 126 MB "
+                  "L2 across the step's 12+ GEMMs"}
 
 
 def bind_numa_local(device: int):
@@ -272,76 +288,78 @@ def bind_numa_local(device: int):
         return None
 
 
+# ------------------------------------------------------------------ configurations
+# Default workloads per GPU count (BASELINE.json configs).
+#   N = 1: C2, the GPT-5B block on 1x1x1x1 (configs[1]).
+#   N = 8: C3 exactly: the GPT-20B block, m = 16384 global tokens, 2x2x2x1.
+#   N = 4: the C3 proxy (2,2,1,1) at m = 8192: every rank runs C3's local GEMM
+#          shapes and C3's AR_x / AR_y message sizes (one Z level fewer).
+#   N = 2: (2,1,1,1) at m = 4096: C3's per-GPU flops on a 2-GPU tensor grid.
+# Per-GPU work is C3's at N = 2, 4, 8 (weak scaling of the C3 workload).
+# Sub-records of the same JSON line (N = 4 proxies / N = 8 exact): C4a / C4b
+# (80B, the model's phase-B pair 1x4x2 and 2x4x1) and C5 (40B,
+# 2x2x1 x Gd=2), plus the data-parallel weak-scaling line (5B block, 16384
+# tokens per GPU, the grid the performance model ranks first).
+PRIMARY = {
+    1: dict(label="C2", model="5B", m=16384, grid=(1, 1, 1, 1), phase="A"),
+    2: dict(label="C3 family at N=2 (C3's per-GPU flops)", model="20B", m=4096,
+            grid=(2, 1, 1, 1), phase="A"),
+    4: dict(label="C3 proxy (C3's local shapes and AR sizes)", model="20B", m=8192,
+            grid=(2, 2, 1, 1), phase="A"),
+    8: dict(label="C3", model="20B", m=16384, grid=(2, 2, 2, 1), phase="A"),
+}
+SUB = {
+    4: [dict(label="C4a proxy (80B, phase B)", model="80B", m=16384, grid=(1, 2, 2, 1), phase="B"),
+        dict(label="C4b proxy (80B, phase B)", model="80B", m=16384, grid=(2, 2, 1, 1), phase="B"),
+        dict(label="C5 proxy (40B, tensor x data)", model="40B", m=16384, grid=(2, 1, 1, 2),
+             phase="A")],
+    8: [dict(label="C4a", model="80B", m=16384, grid=(1, 4, 2, 1), phase="B"),
+        dict(label="C4b", model="80B", m=16384, grid=(2, 4, 1, 1), phase="B"),
+        dict(label="C5", model="40B", m=16384, grid=(2, 2, 1, 2), phase="A")],
+}
+
+
+def case1_table(path=None):
+    """Measured Case-1 database for grid selection:
+    {(G0, G1): bytes/s}.  Entries missing from the measured file (e.g. the
+    8-GPU groups of a 4-GPU measurement) take the mean of the measured ones;
+    with no file, uniform 1e11 (Case 1 with equal beta).  Returns (table, source)."""
+    path = path or os.path.join(ROOT, "profiles", "case1_table.json")
+    full = [(g0, g1) for g0 in range(1, 9) for g1 in range(2, 9) if g0 * g1 <= 8]
+    if os.path.exists(path):
+        d = json.load(open(path))
+        meas = {tuple(int(x) for x in k.split(",")): float(v) * 1e9
+                for k, v in d["beta_GBps"].items()}
+        fill = sum(meas.values()) / len(meas)
+        return ({k: meas.get(k, fill) for k in full},
+                f"measured {os.path.relpath(path, ROOT)} ({len(meas)} entries; others = their mean)")
+    return {k: 1.0e11 for k in full}, "uniform beta 1e11 (no measured table)"
+
+
+def model_top1(ax, layers, world, fixed_gd=0):
+    tb, src = case1_table()
+    best = ax.axonn_grid_select(layers, world, 8, tb, 1.0e11, 2, fixed_gd, cap=1)[0]
+    return (best["gx"], best["gy"], best["gz"], best["gd"]), src
+
+
 # ------------------------------------------------------------------ GPU arm
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="axonn", choices=["axonn", "reference"])
-    ap.add_argument("--grid", default=None, help="gx,gy,gz,gd (default: model-selected)")
-    ap.add_argument("--model", default="5B", choices=sorted(HIDDEN))
-    ap.add_argument("--tokens-per-gpu", type=int, default=16384,
-                    help="global m = tokens-per-gpu x N (BASELINE.json: 16384)")
-    ap.add_argument("--chunks", type=int, default=4, help="forward AR pipelining chunks")
-    ap.add_argument("--gemm-sms", type=int, default=0, help="SM budget of the GEMM grid (0 = all)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--graph", action="store_true",
-                    help="capture one step in a CUDA graph and time its replays")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--w-init", default="scaled", choices=["scaled", "uniform"],
-                    help="weights U(+-sqrt(3/k)) (random init) or U(-1,1)")
-    ap.add_argument("--blocks", type=int, default=1,
-                    help="GPT blocks per step, chained fc2 -> next QKV (SURVEY.md §8(f) f-1)")
-    ap.add_argument("--grad-f32", action="store_true",
-                    help="AXONN_BF16_GRADF32: dW in fp32, RS_z / data-parallel sums in fp32 (R17)")
-    ap.add_argument("--recompute", action="store_true",
-                    help="activation checkpointing (PAPER.md:722-723): each layer's forward re-runs "
-                         "before its backward; flops counted 8mkn as Narayanan et al.'s formula does")
-    ap.add_argument("--no-chain", action="store_true",
-                    help="independent per-layer inputs (default: proj->fc1->fc2 chained)")
-    args = ap.parse_args()
-    # Exactly one JSON line on stdout: libraries (NCCL prints its version line)
-    # write to fd 1, so fd 1 is pointed at stderr and the JSON goes to a copy.
-    out_fd = os.dup(1)
-    os.dup2(2, 1)
-    global _JSON_OUT
-    _JSON_OUT = os.fdopen(out_fd, "w")
-    if args.impl == "reference":
-        run_reference(args)
-        return
+class Ctx:
+    pass
 
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import paper_2502_08145_b200 as ax
 
-    h = HIDDEN[args.model]
-    m = args.tokens_per_gpu * world
-    layers = block_layers(h, m) * args.blocks
-    if args.grid:
-        grid = tuple(int(x) for x in args.grid.split(","))
-    elif world == 1:
-        grid = (1, 1, 1, 1)
-    else:
-        tb = {(g0, g1): 1.0e11 for g0 in range(1, 9) for g1 in range(2, 9) if g0 * g1 <= 8}
-        best = ax.axonn_grid_select(layers, world, 8, tb, 1.0e11, 2, 0, cap=1)[0]
-        grid = (best["gx"], best["gy"], best["gz"], best["gd"])
-
-    if world > 1:
-        ax.bootstrap_from_torch_distributed(local)
+def run_config(c, spec, steps, warmup, e2e_on, exposure_on):
+    """Time one workload: `spec` = dict(model, m (global tokens), grid, phase,
+    blocks, chain, label).  Returns the record (value, overlap, e2e, ...)."""
+    ax, torch, dist, args = c.ax, c.torch, c.dist, c.args
+    world, rank, local = c.world, c.rank, c.local
+    h = HIDDEN[spec["model"]]
+    m = spec["m"]
+    grid = tuple(spec["grid"])
+    blocks = spec.get("blocks", 1)
+    chain = spec.get("chain", True)
+    layers = block_layers(h, m, spec.get("phase", "A")) * blocks
     ax.axonn_grid_init(*grid)
-    if args.gemm_sms:
-        ax.axonn_set_gemm_sms(args.gemm_sms)
-
-    stream = torch.cuda.Stream()
+    stream = c.stream
     gen = torch.Generator(device="cuda")
     gen.manual_seed(42 + rank)
     bf = torch.bfloat16
@@ -351,7 +369,6 @@ def main():
         t.uniform_(-scale, scale, generator=gen)
         return t.to(bf)
 
-    chain = not args.no_chain
     gdt = torch.float32 if args.grad_f32 else bf   # dŴ storage
     gsz = 4 if args.grad_f32 else 2
     gcode = ax.AXONN_BF16_GRADF32 if args.grad_f32 else ax.AXONN_BF16  # dW product dtype
@@ -376,8 +393,8 @@ def main():
                 rec[key] = ptr
         L.append(rec)
     # inputs: external (uniform(-1,1), uploaded by e2e) or chained
-    # chained: inside a block proj -> fc1 -> fc2; across blocks fc2 (transposed,
-    # columns over Y) -> the next block's QKV (normal, input columns over Y).
+    # chained: inside a block proj -> fc1 -> fc2; across blocks fc2 -> the next
+    # block's QKV (alternating normal/transposed layers share shard layouts).
     # External: the first QKV input, every proj input (attention output), the
     # last fc2's dO (loss gradient) and every QKV dO (attention backward).
     nL = len(layers)
@@ -421,9 +438,18 @@ def main():
 
     ax.axonn_comm_bytes(reset=True)
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             step(stream)
     barrier()
+    if args.soak > 0:
+        # untimed steps until the power cap has settled the clocks (the
+        # default stays 0: the timed region is exactly --steps steps)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            while time.perf_counter() - t0 < args.soak:
+                step(stream)
+                torch.cuda.synchronize()
+        barrier()
 
     # ---------------------------------------------------------------- timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -442,6 +468,7 @@ def main():
         for _ in range(2):
             graph.replay()
         barrier()
+    ax.axonn_comm_bytes(reset=True)
     launches0 = ax.axonn_kernel_launches()
     if not args.graph:
         ax.axonn_profile_read()
@@ -450,7 +477,7 @@ def main():
         barrier()
         ev0.record(stream)
         with torch.cuda.stream(stream):
-            for _ in range(args.steps):
+            for _ in range(steps):
                 if graph is not None:
                     graph.replay()
                 else:
@@ -460,41 +487,33 @@ def main():
     ax.axonn_profile_enable(False)
     launches = ax.axonn_kernel_launches() - launches0
     if graph is not None:
-        launches = per_step_launches * args.steps
+        launches = per_step_launches * steps
     comm0 = ax.axonn_comm_bytes(reset=True)
     gemm_n, gemm_ms, gemm_flops = ax.axonn_profile_read()
     if graph is not None:  # events captured once hold the last replay: one step
-        gemm_n, gemm_ms, gemm_flops = gemm_n * args.steps, gemm_ms * args.steps, gemm_flops * args.steps
-    t_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+        gemm_n, gemm_ms, gemm_flops = gemm_n * steps, gemm_ms * steps, gemm_flops * steps
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1)) / steps
     # whole job (all ranks): 6mkn per layer, 8mkn with recomputation
     flops_step = model_flops(layers) * (8.0 / 6.0 if args.recompute else 1.0)
     value = flops_step / (t_ms * 1e-3) / 1e12
-
-    peaks, peaks_src = read_peaks()
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
-    peak = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
-    burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tf):
-        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+    clocks = clk.summary()
 
     # ---------------------------------------------------------------- e2e
     e2e = None
-    if not args.no_e2e:
+    if e2e_on:
         cpus0 = os.sched_getaffinity(0)
         numa_cpus = bind_numa_local(local)
         # Host buffers: each step uploads the block's external inputs (pinned;
-        # with --no-chain every layer's I and dO) and reads every dW back.
-        # Device inputs are double-buffered so step s+1's uploads (copy stream,
-        # in consumption order) overlap step s's compute; read-backs run on a
-        # third stream (PCIe is full duplex).
+        # with --no-chain every layer's I and dO) and reads the step's results
+        # back: every dŴ, the block output O (last fc2) and the block input
+        # gradient dX (first QKV's dI).  Device inputs are double-buffered so
+        # step s+1's uploads (copy stream, in consumption order) overlap step
+        # s's compute; read-backs run on a third stream (PCIe is full duplex).
         hI = {i: L[i]["I"].cpu().pin_memory() for i in ext_I}
         hdO = {i: L[i]["dO"].cpu().pin_memory() for i in ext_dO}
-        # the step's result, the weight gradient, crosses to the host once:
-        # the Gd data-parallel replicas hold identical dŴ, so each reads back
-        # the 1/Gd slice its DATA coordinate selects (the union over ranks is
-        # every dŴ element exactly once)
+        # the weight gradient crosses to the host once: the Gd data-parallel
+        # replicas hold identical dŴ, so each reads back the 1/Gd slice its
+        # DATA coordinate selects (the union over ranks is every dŴ element once)
         _, _, _, dcoord = ax.axonn_grid_coords()
         gd = grid[3]
         wsl = []
@@ -503,6 +522,9 @@ def main():
             lo, hi = S_ * dcoord // gd, S_ * (dcoord + 1) // gd
             wsl.append((lo, hi))
         hdW = [torch.empty(hi - lo, dtype=gdt).pin_memory() for lo, hi in wsl]
+        gl, g0_ = L[-1]["g"], L[0]["g"]
+        hO = torch.empty(gl.m_l * gl.n_l, dtype=bf).pin_memory()    # block output O
+        hdX = torch.empty(g0_.m_l * g0_.k_l, dtype=bf).pin_memory()  # block input gradient
         dev_sets = [[(l["I"], l["dO"]) for l in L],
                     [(torch.empty_like(L[i]["I"]) if i in ext_I else L[i]["I"],
                       torch.empty_like(L[i]["dO"]) if i in ext_dO else L[i]["dO"])
@@ -512,12 +534,19 @@ def main():
         evO = [[torch.cuda.Event() for _ in L] for _ in range(2)]
         ev_free = [torch.cuda.Event(), torch.cuda.Event()]
         ev_done = torch.cuda.Event()
+        ev_fwd = torch.cuda.Event()
         ev_read = [torch.cuda.Event() for _ in L]
+        ev_readO, ev_readX = torch.cuda.Event(), torch.cuda.Event()
         bi = sum(t.numel() * 2 for t in list(hI.values()) + list(hdO.values()))
-        bo = sum(t.numel() * gsz for t in hdW)
-        # whole job: the slices' union is every weight-gradient element once
-        bo_total = sum(gsz * k * n for (_, k, n, _) in layers)
-        assert world > 1 or bo == bo_total
+        bo = sum(t.numel() * gsz for t in hdW) + 2 * (hO.numel() + hdX.numel())
+
+        def raw_read(dst_t, src, nbytes, off=0):
+            if isinstance(src, int):
+                copy_raw(dst_t.data_ptr(), src + off, nbytes, down)
+            else:
+                dst_t.copy_(src.reshape(-1)[off // dst_t.element_size():
+                                            (off + nbytes) // dst_t.element_size()],
+                            non_blocking=True)
 
         def upload(s_idx):
             b = s_idx % 2
@@ -538,11 +567,16 @@ def main():
                         ax.axonn_fc_prefetch(L[i + 1]["h"], L[i + 1]["W"], stream)
                     if i in ext_I:
                         stream.wait_event(evI[b][i])
+                    if i == len(L) - 1:
+                        stream.wait_event(ev_readO)  # previous step's O has reached the host
                     ax.axonn_fc_forward(l["h"], dev_sets[b][i][0], l["W"], l["O"], stream)
+                ev_fwd.record(stream)
                 for i in reversed(range(len(L))):
                     if i in ext_dO:
                         stream.wait_event(evO[b][i])
                     stream.wait_event(ev_read[i])    # previous step's dŴ has reached the host
+                    if i == 0:
+                        stream.wait_event(ev_readX)
                     if args.recompute:
                         ax.axonn_fc_forward(L[i]["h"], dev_sets[b][i][0], L[i]["W"], L[i]["O"],
                                             stream)
@@ -551,14 +585,14 @@ def main():
                 ev_free[b].record(stream)
                 ev_done.record(stream)
             with torch.cuda.stream(down):
+                down.wait_event(ev_fwd)              # the block output, during the backward
+                raw_read(hO, L[-1]["O"], 2 * hO.numel())
+                ev_readO.record(down)
                 down.wait_event(ev_done)
+                raw_read(hdX, L[0]["dI"], 2 * hdX.numel())
+                ev_readX.record(down)
                 for i in reversed(range(len(L))):    # in the next step's backward order
-                    l = L[i]
-                    if isinstance(l["dW"], int):
-                        copy_raw(hdW[i].data_ptr(), l["dW"] + gsz * wsl[i][0], hdW[i].numel() * gsz,
-                                 down)
-                    else:
-                        hdW[i].copy_(l["dW"][wsl[i][0]:wsl[i][1]], non_blocking=True)
+                    raw_read(hdW[i], L[i]["dW"], hdW[i].numel() * gsz, gsz * wsl[i][0])
                     ev_read[i].record(down)
 
         def e2e_run(n):
@@ -570,7 +604,7 @@ def main():
 
         e2e_run(2)
         barrier()
-        ksteps = max(3, min(args.steps, 10))
+        ksteps = max(3, min(steps, 10))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
@@ -584,21 +618,23 @@ def main():
         barrier()
         te = max_over_ranks(e0.elapsed_time(e1)) / ksteps
         e2e = {"value": flops_step / (te * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo_total,
+               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world,
                "ms_per_step": te, "steps": ksteps,
                "numa_local_cpus": numa_cpus,
                "inputs": ("block input X, attention output (proj input), loss gradient at fc2 "
                           "output, attention-backward gradient at QKV output; proj->fc1->fc2 chained "
                           "on device (PAPER.md:402-414)") if chain else "every layer's I and dO",
+               "outputs": ("every weight gradient dŴ (each data-parallel replica its 1/Gd slice), "
+                           "the block output O (last fc2's output shard) and the block input "
+                           "gradient dX (first QKV's dI shard), per rank"),
                "path": "pinned host -> device uploads (double-buffered, copy stream) + "
-                       "axonn_fc_forward/backward + grads_sync + dW device->host (third stream),"
-                       " all inside the timed region"}
-
-        os.sched_setaffinity(0, cpus0)   # the CPU baseline below uses every core
+                       "axonn_fc_forward/backward + grads_sync + results device->host (third "
+                       "stream), all inside the timed region"}
+        os.sched_setaffinity(0, cpus0)   # the CPU baseline uses every core
 
     # ---------------------------------------------------------------- GEMM-only (exposed comm)
     exposed = None
-    if world > 1:
+    if exposure_on and world > 1:
         scratch = []
         for l, (_, k_glob, _, _) in zip(L, layers):
             g = l["g"]
@@ -620,17 +656,17 @@ def main():
         barrier()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             gemm_step(stream)
         g1.record(stream)
         barrier()
-        t_gemm = max_over_ranks(g0.elapsed_time(g1)) / args.steps
+        t_gemm = max_over_ranks(g0.elapsed_time(g1)) / steps
 
         # per layer: Alg. 1 forward / backward through the ABI vs the same
         # local products alone (SURVEY.md §8(d) "per layer and per block")
-        names = [["qkv", "proj", "fc1", "fc2"][i % 4] + (f"{i // 4}" if args.blocks > 1 else "")
+        names = [["qkv", "proj", "fc1", "fc2"][i % 4] + (f"{i // 4}" if blocks > 1 else "")
                  for i in range(nL)]
-        nrep = max(3, min(args.steps, 20))
+        nrep = max(3, min(steps, 20))
         ev = {key: [torch.cuda.Event(enable_timing=True) for _ in range(2 * nrep)]
               for key in [f"{n_}_{ph}" for n_ in names for ph in ("fwd", "bwd", "fwd_gemm", "bwd_gemm")]
               + ["sync"]}
@@ -672,47 +708,190 @@ def main():
         per_layer["grads_sync"] = {"ms": acc_ms["sync"]}
         exposed = {"t_step_ms": t_ms, "t_gemm_only_ms": t_gemm, "per_layer": per_layer,
                    "exposed_comm_frac": max(0.0, (t_ms - t_gemm) / t_ms),
-                   "comm_bytes_per_rank_per_step": {k: v // max(1, args.steps + args.warmup)
-                                                    for k, v in comm0.items()}}
+                   "comm_bytes_per_rank_per_step": {k: v // max(1, steps)
+                                                    for k, v in comm0.items()},
+                   "comm_bytes_note": "bytes the collectives of one step send per rank "
+                                      "(ring formulas of Eqs. 1-5 on the element counts issued)"}
+    fused = {a: ax.axonn_fused_status(a) for a in ("x", "y", "z", "d")}
+    for l in L:
+        ax.axonn_fc_destroy(l["h"])
+    ax.axonn_grid_finalize()
+    del L
+    torch.cuda.empty_cache()
+    rec = {"label": spec.get("label", ""), "value": value, "per_gpu_tflops": value / world,
+           "ms_per_step": t_ms, "steps": steps, "warmup": warmup,
+           "config": {**workload_config(spec["model"], world, grid, m, blocks, spec.get("phase", "A")),
+                      "chained": chain, "recompute": bool(args.recompute),
+                      "grad_f32": bool(args.grad_f32),
+                      "flops_per_layer": "8mkn (forward recomputed)" if args.recompute else "6mkn"},
+           "gpu_launches": launches, "overlap": exposed, "clocks": clocks, "e2e": e2e,
+           "fused_axes": fused,
+           "gemm": {"launches": gemm_n, "ms": gemm_ms, "flops": gemm_flops}}
+    if "grid_source" in spec:
+        rec["config"]["grid_source"] = spec["grid_source"]
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="axonn", choices=["axonn", "reference"])
+    ap.add_argument("--grid", default=None, help="gx,gy,gz,gd (default: per-N plan, see PRIMARY)")
+    ap.add_argument("--model", default=None, choices=sorted(HIDDEN))
+    ap.add_argument("--tokens", type=int, default=None, help="global m (default: per-N plan)")
+    ap.add_argument("--tokens-per-gpu", type=int, default=None,
+                    help="global m = tokens-per-gpu x N (the data-parallel weak-scaling family)")
+    ap.add_argument("--phase", default=None, choices=["A", "B"])
+    ap.add_argument("--chunks", type=int, default=4, help="forward AR pipelining chunks")
+    ap.add_argument("--gemm-sms", type=int, default=0, help="SM budget of the GEMM grid (0 = all)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the sub-records (C4a/C4b/C5, DP)")
+    ap.add_argument("--sub-steps", type=int, default=20, help="timed steps of each sub-record")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one step in a CUDA graph and time its replays")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--soak", type=float, default=0.0,
+                    help="untimed seconds of steps before timing (settles the power-capped clock)")
+    ap.add_argument("--w-init", default="scaled", choices=["scaled", "uniform"],
+                    help="weights U(+-sqrt(3/k)) (random init) or U(-1,1)")
+    ap.add_argument("--blocks", type=int, default=1,
+                    help="GPT blocks per step, chained fc2 -> next QKV (SURVEY.md §8(f) f-1)")
+    ap.add_argument("--grad-f32", action="store_true",
+                    help="AXONN_BF16_GRADF32: dW in fp32, RS_z / data-parallel sums in fp32 (R17)")
+    ap.add_argument("--recompute", action="store_true",
+                    help="activation checkpointing (PAPER.md:722-723): each layer's forward re-runs "
+                         "before its backward; flops counted 8mkn as Narayanan et al.'s formula does")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="independent per-layer inputs (default: proj->fc1->fc2 chained)")
+    args = ap.parse_args()
+    # Exactly one JSON line on stdout: libraries (NCCL prints its version line)
+    # write to fd 1, so fd 1 is pointed at stderr and the JSON goes to a copy.
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(out_fd, "w")
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2502_08145_b200 as ax
+    if world > 1:
+        ax.bootstrap_from_torch_distributed(local)
+    if args.gemm_sms:
+        ax.axonn_set_gemm_sms(args.gemm_sms)
+    c = Ctx()
+    c.ax, c.torch, c.dist, c.args = ax, torch, dist, args
+    c.world, c.rank, c.local = world, rank, local
+    c.stream = torch.cuda.Stream()
+
+    # the primary workload: the per-N plan, unless overridden
+    default = PRIMARY.get(world)
+    custom = (args.grid or args.model or args.tokens or args.tokens_per_gpu or args.phase
+              or default is None)
+    if custom:
+        model = args.model or "5B"
+        m = (args.tokens if args.tokens else (args.tokens_per_gpu or 16384) * world)
+        phase = args.phase or "A"
+        spec = dict(label="custom", model=model, m=m, phase=phase)
+        if args.grid:
+            spec["grid"] = tuple(int(x) for x in args.grid.split(","))
+        elif world == 1:
+            spec["grid"] = (1, 1, 1, 1)
+        else:
+            spec["grid"], spec["grid_source"] = model_top1(ax, block_layers(HIDDEN[model], m, phase), world)
+    else:
+        spec = dict(default)
+    spec["blocks"] = args.blocks
+    spec["chain"] = not args.no_chain
+    prim = run_config(c, spec, args.steps, args.warmup, not args.no_e2e, True)
+
+    subs = []
+    if not args.no_sub and not custom and world > 1:
+        plan = [dict(s) for s in SUB.get(world, [])]
+        # the data-parallel weak-scaling line: 5B block, 16384 tokens per GPU,
+        # the model's top-ranked grid (round-1 headline, kept as a sub-record)
+        dp_layers = block_layers(HIDDEN["5B"], 16384 * world)
+        g, src = model_top1(ax, dp_layers, world)
+        plan.append(dict(label="data-parallel weak scaling (5B, 16384 tokens/GPU, model top-1)",
+                         model="5B", m=16384 * world, grid=g, phase="A", grid_source=src))
+        for sp in plan:
+            sp["blocks"], sp["chain"] = 1, not args.no_chain
+            r = run_config(c, sp, args.sub_steps, max(3, args.warmup), False, True)
+            subs.append({k: r[k] for k in ("label", "value", "per_gpu_tflops", "ms_per_step",
+                                           "steps", "config", "overlap", "clocks",
+                                           "gpu_launches", "fused_axes")})
+
+    peaks, peaks_src = read_peaks()
+    gemm_n, gemm_ms, gemm_flops = prim["gemm"]["launches"], prim["gemm"]["ms"], prim["gemm"]["flops"]
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    sustained = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
+    burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+    # The measured peaks are cuBLAS at burst clocks (best of 10) and back to
+    # back for 4 s (sustained, power-capped).  The timed region is judged by
+    # its own clock: median SM clock within 3% of the maximum -> burst peak.
+    clk = prim["clocks"]
+    at_max = bool(clk.get("sm_mhz") and clk.get("sm_max_mhz")
+                  and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"])
+    peak = burst if at_max else sustained
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, thr, desc = oracle_sample(h, 2048, 10.0)
+        v, thr, desc = oracle_sample(HIDDEN[spec["model"]], 2048, 10.0)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": desc}
 
     if rank == 0:
+        value = prim["value"]
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": prim["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": ("synthetic (inputs uniform(-1,1) bf16, weights "
                      + ("U(+-sqrt(3/k)) random init" if args.w_init == "scaled" else "U(-1,1)")
                      + ", device-generated, seeded)"),
-            "config": {**workload_config(args.model, world, grid, args.tokens_per_gpu, args.blocks),
-                       "chained": chain, "recompute": bool(args.recompute),
-                       "grad_f32": bool(args.grad_f32),
-                       "flops_per_layer": "8mkn (forward recomputed)" if args.recompute else "6mkn"},
+            "config": {**prim["config"], "label": prim["label"]},
             "per_gpu_tflops": value / world,
             "frac_of_peak": {"advertised_2250": value / world / 2250.0,
                              "measured_burst": value / world / burst,
-                             "measured_sustained": value / world / peak, "peaks": peaks_src},
+                             "measured_sustained": value / world / sustained, "peaks": peaks_src},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
-                         "kernel": "gemm_bf16_tcgen05 (all NN/NT/TN launches of the timed region;"
-                                   " achieved = sum 2MNK / sum event time)",
-                         "peak_kind": f"bf16_tflops_sustained, {peaks_src}",
+                         "kernel": "gemm_bf16_tcgen05_pair (all NN/NT/TN launches of the timed "
+                                   "region; achieved = sum 2MNK / sum event time on the launching "
+                                   "stream)",
+                         "peak_kind": ("bf16_tflops (burst: the window's median SM clock is at its "
+                                       "maximum)" if at_max else
+                                       "bf16_tflops_sustained (the window ran below max clock)")
+                                      + f", {peaks_src}",
                          "frac_of_burst": achieved / burst if burst else None,
+                         "frac_of_sustained": achieved / sustained if sustained else None,
                          "gemm_launches": gemm_n, "gemm_ms_per_step": gemm_ms / args.steps},
             "cuda_graph": bool(args.graph),
-            "gpu_launches": launches,
-            "overlap": exposed,
-            "clocks": clk.summary(),
-            "e2e": e2e,
+            "gpu_launches": prim["gpu_launches"],
+            "overlap": prim["overlap"],
+            "fused_axes": prim["fused_axes"],
+            "clocks": prim["clocks"],
+            "e2e": prim["e2e"],
             "cpu_baseline": cpu,
+            "sub_records": subs or None,
         }
         emit(out)
-    ax.axonn_grid_finalize()
     if world > 1:
         dist.destroy_process_group()
 

@@ -232,6 +232,51 @@ axonn_status_t axonn_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K,
                           void* C, int64_t ldc, void* stream);
 
 /* ======================================================================== */
+/* Test support: the fused collectives of the multi-GPU path on ONE GPU.     */
+/* ======================================================================== */
+/* Runs Alg. 1 (forward, backward, RS_z and the data-parallel sum;           */
+/* PAPER.md:375-390, 313-317) for EVERY rank of the grid (gx,gy,gz,gd) on    */
+/* the current device, with the same device code that moves data between    */
+/* ranks on NVLink: GEMM epilogues that multimem.red into a multicast buffer */
+/* or scatter 16-B units into the owners' receive slots, the owner phase     */
+/* that sums the slots in rank order and broadcasts (multimem.st, or plain   */
+/* stores to the peer on 2-rank axes) or re-scatters to the DATA owners, and */
+/* the Z all-gather by copy engines or SM pull.  Every rank's "symmetric"    */
+/* buffers are allocated side by side on this device; stream order replaces  */
+/* the cross-rank barriers; multicast uses a one-device multicast object     */
+/* (its single copy is then copied to each member, as NVSwitch replicates).  */
+/* Arrays hold one pointer per rank r = 0..G-1 (host arrays of device        */
+/* pointers, laid out as for axonn_fc_forward/backward with rank r's shard   */
+/* geometry: axonn_shard_geometry).  Device-synchronous: returns after the   */
+/* step has finished.  `paths` (host, may be NULL) receives the                */
+/* AXONN_LB_PATH_* bits of the fused paths that ran.  Only bf16 and          */
+/* AXONN_BF16_GRADF32 (the fp32 test mode reduces through NCCL).            */
+/* Errors: ARG, CONFIG, SHAPE, CUDA; UNSUPPORTED when a needed collective    */
+/* would not be fused for this shape on the multi-GPU path (it would use     */
+/* NCCL, which has no loopback) or an axis exceeds 8 ranks.                 */
+/* ======================================================================== */
+enum {
+  AXONN_LB_RED_ALWAYS = 1,   /* 2-rank bf16 axes: multimem.red at any K          */
+  AXONN_LB_RED_NEVER = 2,    /* never multimem.red: scatter + owner phase        */
+  AXONN_LB_GATHER_PULL = 4,  /* AG_z by the SM pull kernel (else copy engines)   */
+  AXONN_LB_EMULATE_MC = 8    /* no multicast object: red.global.add / plain st   */
+};
+enum {
+  AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,
+  AXONN_LB_PATH_BWD_RED = 4, AXONN_LB_PATH_BWD_SCATTER = 8,
+  AXONN_LB_PATH_RS_Z = 16,
+  AXONN_LB_PATH_DP_RED = 32, AXONN_LB_PATH_DP_SCATTER = 64,
+  AXONN_LB_PATH_DP_AFTER_RS = 128,
+  AXONN_LB_PATH_GATHER_COPY = 256, AXONN_LB_PATH_GATHER_PULL = 512,
+  AXONN_LB_PATH_MULTICAST = 1024   /* a real one-device multicast object was used */
+};
+axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
+                                   const void* const* I_local, const void* const* W_hat,
+                                   const void* const* dO_local, void* const* O_local,
+                                   void* const* dI_local, void* const* dW_hat, int flags,
+                                   void* stream, int* paths);
+
+/* ======================================================================== */
 /* Instrumentation: CUDA events around every GEMM launch on its launching    */
 /* stream, and a count of every kernel this library launched.                */
 /* ======================================================================== */
@@ -281,7 +326,8 @@ typedef struct {
 
 /* Enumerate every (gx,gy,gz,gd) with product G (gd fixed when fixed_gd > 0),
  * drop those that do not divide every layer, score by Eq. 6 summed over
- * layers with b = bytes_per_elem, sort ascending with ties (relative 1e-12)
+ * layers with b = bytes_per_elem, sort ascending on t_comm rounded to 12
+ * significant digits, ties
  * broken lexicographically on (gx,gy,gz,gd) (reading R12), and write the
  * first min(cap, count) to `out` (host).  *n_out = total feasible count.
  * Errors: ARG, CONFIG (a needed Case-1 table entry is missing; the message

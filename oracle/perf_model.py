@@ -48,6 +48,8 @@ def gpt_block(h: int, m: int, phase: str = "A"):
     Phase A transposes proj and fc2; phase B transposes QKV and fc1
     (reading R2b: the paper fixes only the alternation).
     """
+    if phase not in ("A", "B"):
+        raise ValueError(f"phase must be 'A' or 'B' (reading R2b), got {phase!r}")
     shapes = [(h, 3 * h), (h, h), (h, 4 * h), (4 * h, h)]
     flags = [False, True, False, True] if phase == "A" else [True, False, True, False]
     return [Layer(m, k, n, t) for (k, n), t in zip(shapes, flags)]

@@ -30,6 +30,10 @@ AXONN_ERR_INFEASIBLE, AXONN_ERR_CUDA, AXONN_ERR_NCCL, AXONN_ERR_UNSUPPORTED = 5,
 AXONN_BF16, AXONN_F32, AXONN_BF16_GRADF32 = 0, 1, 2
 AXONN_OP_NN, AXONN_OP_NT, AXONN_OP_TN = 0, 1, 2
 AXIS = {"x": 0, "y": 1, "z": 2, "d": 3}
+AXONN_LB_RED_ALWAYS, AXONN_LB_RED_NEVER, AXONN_LB_GATHER_PULL, AXONN_LB_EMULATE_MC = 1, 2, 4, 8
+LB_PATHS = {"fwd_red": 1, "fwd_scatter": 2, "bwd_red": 4, "bwd_scatter": 8, "rs_z": 16,
+            "dp_red": 32, "dp_scatter": 64, "dp_after_rs": 128, "gather_copy": 256,
+            "gather_pull": 512, "multicast": 1024}
 _STATUS_NAMES = {0: "OK", 1: "ARG", 2: "CONFIG", 3: "SHAPE", 4: "STATE", 5: "INFEASIBLE",
                  6: "CUDA", 7: "NCCL", 8: "UNSUPPORTED"}
 
@@ -93,6 +97,10 @@ _PROTOS = {
     "axonn_fc_destroy": (_S, [c_void_p]),
     "axonn_gemm": (_S, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                         c_int64, c_void_p, c_int64, c_void_p]),
+    "axonn_loopback_step": (_S, [POINTER(FcDesc), c_int, c_int, c_int, c_int, POINTER(c_void_p),
+                                 POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p),
+                                 POINTER(c_void_p), POINTER(c_void_p), c_int, c_void_p,
+                                 POINTER(c_int)]),
     "axonn_profile_enable": (_S, [c_int]),
     "axonn_profile_read": (_S, [POINTER(c_int64), POINTER(c_double), POINTER(c_double)]),
     "axonn_kernel_launches": (c_int64, []),
@@ -253,6 +261,24 @@ def axonn_fc_destroy(h) -> None:
 def axonn_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, stream=None) -> None:
     _check(_lib.axonn_gemm(op, dtype, M, N, K, _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc,
                            _stream_ptr(stream)))
+
+
+def axonn_loopback_step(m, k, n, cfg, I, W_hat, dO, O, dI, dW, transposed=False,
+                        dtype=AXONN_BF16, flags=0, stream=None) -> set:
+    """Alg. 1 for every rank of grid ``cfg`` on this GPU (include/axonn.h, test
+    support).  I, W_hat, dO, O, dI, dW: per-rank lists of tensors (rank order).
+    Returns the names of the fused paths that ran (LB_PATHS)."""
+    G = cfg[0] * cfg[1] * cfg[2] * cfg[3]
+    arrs = []
+    for lst in (I, W_hat, dO, O, dI, dW):
+        if len(lst) != G:
+            raise ValueError(f"need {G} per-rank tensors, got {len(lst)}")
+        arrs.append((c_void_p * G)(*[_ptr(t).value or 0 for t in lst]))
+    d = _desc(m, k, n, transposed, dtype)
+    paths = c_int()
+    _check(_lib.axonn_loopback_step(byref(d), *cfg, *arrs, flags, _stream_ptr(stream),
+                                    byref(paths)))
+    return {name for name, bit in LB_PATHS.items() if paths.value & bit}
 
 
 def axonn_profile_enable(enabled: bool = True) -> None:

@@ -37,6 +37,7 @@
 #include "../../include/axonn.h"
 #include "gemm.h"
 #include "perf_model.h"
+#include "runtime.h"
 #include "sym.h"
 
 namespace {
@@ -238,7 +239,8 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
                                      ? "gemm: fp32 output is implemented for op 2 (TN) only"
                                      : "gemm: op must be 0 (NN), 1 (NT) or 2 (TN)");
     default: {
-      cudaError_t e = cudaGetLastError();
+      cudaError_t e = axonn::gemm_last_launch_error();
+      if (e == cudaSuccess) e = cudaGetLastError();
       return fail(AXONN_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(e));
     }
   }
@@ -333,6 +335,8 @@ struct axonn_fc {
   Fused fi;   // dI  over the backward axis     (line 12 fused into line 11)
   Fused fw;   // dŴ  over DATA when Gz == 1     (PAPER.md:313-317 fused into line 13)
   Fused fz;   // RS_z fused into line 13: the epilogue scatters to the slice owners
+  Fused fd;   // dŴ over DATA when Gz > 1: the RS_z owner phase scatters its reduced
+              // slice to the DATA owners (PAPER.md:313-317 fused into line 14)
   axonn::SymBuf wstage;        // AG_z over copy engines: symmetric staging copy of Ŵ
   std::vector<void*> wpeer;    // every Z rank's staging address (LSA)
   std::string fused_why;            // non-empty: fused buffers fell back to NCCL
@@ -351,7 +355,7 @@ axonn_status_t fused_barrier(int axis, cudaStream_t st, int index) {
   return AXONN_OK;
 }
 
-// Fused all-reduce of a rows x cols bf16 output over `axis` (see sym.cu):
+// Fused all-reduce of a rows x cols output over `axis` (see sym.cu):
 // 2 ranks: multimem.red straight from the epilogue (RNE(a + b), exact
 // commutative: bit-identical to NCCL); P >= 3: the epilogue scatters 16-B
 // vectors to their owner rank, the owner sums the P slots in rank order and
@@ -362,48 +366,77 @@ axonn_status_t fused_barrier(int axis, cudaStream_t st, int index) {
 // (K >= AXONN_RED_MIN_K, default 8192): fully overlapped, no extra pass.
 // Shorter K (e.g. the transposed proj layer, K = h/Gx) uses the scatter mode,
 // whose epilogue traffic is half as large and goes out as plain stores.
-bool fused_setup(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_t kdim,
-                 std::string* why, int es = 2) {
+//
+// Buffers are created in two phases: fused_plan records the
+// symmetric buffers a layer needs; axonn_fc_create allocates them locally,
+// agrees on the outcome over the world, and only then registers the windows
+// (collective), so every rank makes the same sequence of collective calls.
+struct SymReq {
+  int axis;
+  size_t bytes;
+  axonn::SymBuf* buf;
+};
+
+void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_t kdim, int es,
+                std::vector<SymReq>* reqs) {
   f->axis = axis;
   f->es = es;
   f->epi = axonn::EpiTarget();
-  const int P = S.g[axis];
-  const int64_t n = rows * cols;
-  const int unit = 16 / es;  // elements per 16-B epilogue unit
-  // NCCL path: no window, a 1-rank axis, an empty output, 8-element rows not
-  // possible, or an empty product (K == 0 writes zeros; nothing to scatter)
-  if (!S.sym[axis].impl || P < 2 || n <= 0 || cols % unit || kdim <= 0) return true;
-  // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
-  const bool red = es == 2 && P == 2 && kdim >= env_int("AXONN_RED_MIN_K", 8192);
-  if (!red && n % (unit * P)) return true;
-  f->elems = static_cast<size_t>(n);
-  if (!axonn::sym_alloc(&S.sym[axis], f->elems * es, &f->out, why)) return false;
-  if (red) {
-    f->epi.mode = axonn::kMcRed;
-    f->epi.mc = reinterpret_cast<unsigned long long>(f->out.mc);
+  if (!S.sym[axis].impl) return;
+  const int mode = axonn::fused_mode(S.g[axis], es, rows, cols, kdim,
+                                     env_int("AXONN_RED_MIN_K", 8192));
+  if (mode == axonn::kStore) return;
+  f->elems = static_cast<size_t>(rows * cols);
+  f->epi.mode = mode;  // targets are bound after registration (fused_bind)
+  reqs->push_back({axis, f->elems * es, &f->out});
+  if (mode == axonn::kScatter) reqs->push_back({axis, f->elems * es, &f->recv});
+}
+
+// After registration: the epilogue targets (multicast address, or every
+// rank's receive slot) and, on 2-rank scatter axes, the peer's output copy.
+bool fused_bind(axonn_fc::Fused* f, std::string* why) {
+  if (f->epi.mode == axonn::kStore) return true;
+  if (f->epi.mode == axonn::kMcRed) {
+    f->epi = axonn::epi_red(reinterpret_cast<unsigned long long>(f->out.mc));
     return true;
   }
-  if (!axonn::sym_alloc(&S.sym[axis], f->elems * es, &f->recv, why)) return false;
-  f->epi.mode = axonn::kScatter;
-  f->epi.P = P;
-  f->epi.me = S.c[axis];
-  f->epi.slice = n / P;
+  const int P = S.g[f->axis], me = S.c[f->axis];
+  unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < P; ++q) {
-    f->epi.peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv, q));
-    if (!f->epi.peer[q]) {
+    peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv, q));
+    if (!peer[q]) {
       *why = "peer address of the receive window unavailable";
       return false;
     }
   }
+  f->epi = axonn::epi_scatter(P, me, static_cast<long long>(f->elems) / P, peer);
   if (P == 2) {  // the owner sends its reduced slice to the peer with plain stores
-    char* peer_out = static_cast<char*>(axonn::sym_peer_ptr(&f->out, 1 - f->epi.me));
+    char* peer_out = static_cast<char*>(axonn::sym_peer_ptr(&f->out, 1 - me));
     if (!peer_out) {
       *why = "peer address of the output window unavailable";
       return false;
     }
-    f->out_peer = peer_out + static_cast<size_t>(f->epi.me) * f->epi.slice * es;
+    f->out_peer = peer_out + static_cast<size_t>(me) * f->epi.slice * f->es;
   }
   return true;
+}
+
+// Where the owner phase of a scatter-mode reduction writes its slice: its
+// own copy (+ the peer's on 2-rank axes), or every copy through multimem.st.
+axonn::OwnerOut owner_out(const axonn_fc::Fused& f) {
+  axonn::OwnerOut o;
+  const size_t off = static_cast<size_t>(f.epi.me) * f.epi.slice * f.es;
+  if (f.out_peer) {
+    o.mode = axonn::kOwnPlain;
+    o.n_dst = 2;
+    o.dst[0] = reinterpret_cast<unsigned long long>(static_cast<char*>(f.out.ptr) + off);
+    o.dst[1] = reinterpret_cast<unsigned long long>(f.out_peer);
+  } else {
+    o.mode = axonn::kOwnMc;
+    o.n_dst = 1;
+    o.dst[0] = reinterpret_cast<unsigned long long>(f.out.mc) + off;
+  }
+  return o;
 }
 
 axonn_status_t fused_barrier(int axis, cudaStream_t st, int index = 0);
@@ -443,11 +476,8 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
 axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
   STATUS_TRY(fused_barrier(f.axis, st, index));  // every rank's epilogue writes have landed
   if (f.epi.mode == axonn::kScatter) {
-    void* local = nullptr;
-    if (f.out_peer)  // 2 ranks: own copy + plain stores to the peer instead of multicast
-      local = static_cast<char*>(f.out.ptr) + static_cast<size_t>(f.epi.me) * f.epi.slice * f.es;
-    CUDA_TRY(axonn::sym_owner_reduce(&f.recv, &f.out, f.epi.slice, f.epi.P, f.epi.me, S.num_sms,
-                                     st, local, f.out_peer, f.es == 4));
+    CUDA_TRY(axonn::sym_owner_reduce(f.recv.ptr, f.epi.slice, f.epi.P, f.es == 4, owner_out(f),
+                                     S.num_sms, st));
     g_launches.fetch_add(1);
     STATUS_TRY(fused_barrier(f.axis, st, index));  // every owner's broadcast has landed
   }
@@ -489,11 +519,9 @@ axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) 
     STATUS_TRY(fused_barrier(AX_Z, zs));  // peers are done reading my previous staging
     CUDA_TRY(cudaMemcpyAsync(h->wstage.ptr, W_hat, bytes, cudaMemcpyDeviceToDevice, zs));
     STATUS_TRY(fused_barrier(AX_Z, zs));  // every rank's Ŵ is staged
-    for (int q = 0; q < S.g[AX_Z]; ++q) {
-      const void* src = q == S.c[AX_Z] ? W_hat : h->wpeer[q];
-      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(h->wbuf) + q * bytes, src, bytes,
-                               cudaMemcpyDeviceToDevice, zs));
-    }
+    std::vector<const void*> src(S.g[AX_Z]);
+    for (int q = 0; q < S.g[AX_Z]; ++q) src[q] = q == S.c[AX_Z] ? W_hat : h->wpeer[q];
+    CUDA_TRY(axonn::sym_gather_copy(src.data(), S.g[AX_Z], bytes, h->wbuf, zs));
     count_comm(0, S.g[AX_Z], S_el, h->d.dtype);
     CUDA_TRY(cudaEventRecord(h->ev_ag, zs));
     h->prefetched = true;
@@ -508,6 +536,17 @@ axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) 
 }
 
 }  // namespace
+
+namespace axonn {
+axonn_status_t rt_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
+                       int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                       cudaStream_t st, const EpiTarget* epi) {
+  return run_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, st, epi);
+}
+axonn_status_t rt_fail(axonn_status_t s, const char* msg) { return fail(s, "%s", msg); }
+void rt_count_launch() { g_launches.fetch_add(1); }
+int rt_num_sms() { return S.num_sms; }
+}  // namespace axonn
 
 extern "C" {
 
@@ -618,8 +657,6 @@ axonn_status_t axonn_grid_init(int gx, int gy, int gz, int gd) {
       S.sym_why[a].clear();
       if (g[a] > 8)
         S.sym_why[a] = "fused all-reduce implemented for up to 8 ranks";
-      else if (a == AX_D && g[AX_Z] > 1)
-        S.sym_why[a] = "data-parallel all-reduce after a Z reduce-scatter uses NCCL";
       else if (env_int("AXONN_FUSED", 1) == 0)
         S.sym_why[a] = "disabled by AXONN_FUSED=0";
       else
@@ -703,46 +740,78 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
       return cleanup(fail(AXONN_ERR_CUDA, "cudaEventCreate failed"));
   // Fused (NVLS) buffers.  A failure here is not fatal: the layer falls back
   // to NCCL collectives (still the GPU path), but only if EVERY rank does, so
-  // the ranks agree (MIN over the world) before anything is used.
+  // the ranks agree (MIN over the world) before anything is used.  Local
+  // allocations come first and are agreed on before any (collective) window
+  // registration, so a rank that runs out of memory never leaves its peers
+  // waiting inside a registration it will not make.
   std::string why;
-  bool ok = true;
+  std::vector<SymReq> reqs;
+  const int ges = static_cast<int>(elem_size(grad_dtype(desc->dtype)));
   if (desc->dtype != AXONN_F32) {
     // O and dI reduce bf16; dŴ in its gradient precision (fp32 for AXONN_BF16_GRADF32)
-    ok = fused_setup(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, &why) &&
-         fused_setup(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, &why) &&
-         (S.g[AX_Z] > 1 ||
-          fused_setup(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, &why,
-                      static_cast<int>(elem_size(grad_dtype(desc->dtype)))));
+    fused_plan(&h->fo, h->ax_fwd, geo.m_l, geo.n_l, geo.k_l, 2, &reqs);
+    fused_plan(&h->fi, h->ax_bwd, geo.m_l, geo.k_l, geo.n_l, 2, &reqs);
+    if (S.g[AX_Z] == 1) fused_plan(&h->fw, AX_D, geo.k_l, geo.n_l, geo.m_l, ges, &reqs);
   }
-  if (ok && desc->dtype != AXONN_F32 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
+  if (desc->dtype != AXONN_F32 && S.g[AX_Z] > 1 && S.sym[AX_Z].impl && geo.what_len > 0 &&
       geo.what_len % 8 == 0 && geo.m_l > 0) {
-    const int P = S.g[AX_Z];
+    // RS_z fused into the dW epilogue: owner of flat index f is f / S, its Ŵ slice (R4)
     h->fz.axis = AX_Z;
-    h->fz.es = static_cast<int>(elem_size(grad_dtype(desc->dtype)));
+    h->fz.es = ges;
     h->fz.elems = static_cast<size_t>(geo.k_l * geo.n_l);
-    ok = axonn::sym_alloc(&S.sym[AX_Z], h->fz.elems * h->fz.es, &h->fz.recv, &why) &&
-         axonn::sym_alloc(&S.sym[AX_Z], static_cast<size_t>(geo.what_len) * 2, &h->wstage, &why);
-    if (ok) {
-      h->fz.epi.mode = axonn::kScatter;
-      h->fz.epi.P = P;
-      h->fz.epi.me = S.c[AX_Z];
-      h->fz.epi.slice = geo.what_len;  // owner of flat index f is f / S = its Ŵ slice (R4)
+    h->fz.epi.mode = axonn::kScatter;
+    reqs.push_back({AX_Z, h->fz.elems * ges, &h->fz.recv});
+    reqs.push_back({AX_Z, static_cast<size_t>(geo.what_len) * 2, &h->wstage});
+    // the data-parallel sum of dŴ fused behind it: the Z owner phase scatters
+    // its reduced slice to the DATA owners (16-B units of what_len / Gd)
+    const int Pd = S.g[AX_D];
+    if (Pd > 1 && S.sym[AX_D].impl && geo.what_len % (static_cast<int64_t>(16 / ges) * Pd) == 0) {
+      h->fd.axis = AX_D;
+      h->fd.es = ges;
+      h->fd.elems = static_cast<size_t>(geo.what_len);
+      h->fd.epi.mode = axonn::kScatter;
+      reqs.push_back({AX_D, h->fd.elems * ges, &h->fd.recv});
+      reqs.push_back({AX_D, h->fd.elems * ges, &h->fd.out});
+    }
+  }
+  bool ok = true;
+  for (const SymReq& r : reqs) ok = ok && axonn::sym_mem_alloc(r.bytes, r.buf, &why);
+  bool all_ok = ok;
+  axonn_status_t st_agree = agree_all(&all_ok);
+  if (st_agree != AXONN_OK) return cleanup(st_agree);
+  if (all_ok) {
+    // every rank registers every buffer, in the same order, even after a
+    // failure (the calls are collective); the outcome is agreed again
+    bool reg = true;
+    for (const SymReq& r : reqs) {
+      std::string w;
+      if (!axonn::sym_register(&S.sym[r.axis], r.buf, &w) && reg) {
+        reg = false;
+        why = w;
+      }
+    }
+    ok = reg && fused_bind(&h->fo, &why) && fused_bind(&h->fi, &why) && fused_bind(&h->fw, &why);
+    if (ok && h->fz.epi.mode == axonn::kScatter) {
+      const int P = S.g[AX_Z];
+      unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       h->wpeer.resize(P);
       for (int q = 0; q < P && ok; ++q) {
-        h->fz.epi.peer[q] =
-            reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&h->fz.recv, q));
+        peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&h->fz.recv, q));
         h->wpeer[q] = axonn::sym_peer_ptr(&h->wstage, q);
-        if (!h->fz.epi.peer[q] || !h->wpeer[q]) {
+        if (!peer[q] || !h->wpeer[q]) {
           why = "peer address of a Z window unavailable";
           ok = false;
         }
       }
+      if (ok) h->fz.epi = axonn::epi_scatter(P, S.c[AX_Z], geo.what_len, peer);
     }
+    if (ok && h->fd.epi.mode == axonn::kScatter) ok = fused_bind(&h->fd, &why);
+    all_ok = ok;
+    st_agree = agree_all(&all_ok);
+    if (st_agree != AXONN_OK) return cleanup(st_agree);
   }
-  bool all_ok = ok;
-  STATUS_TRY(agree_all(&all_ok));
   if (!all_ok) {
-    for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz}) fused_reset(f);
+    for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz, &h->fd}) fused_reset(f);
     axonn::sym_free(&S.sym[AX_Z], &h->wstage);
     h->wpeer.clear();
     h->fused_why = ok ? "another rank could not allocate its fused buffers" : why;
@@ -765,7 +834,8 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out) {
 
 axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr) {
   if (!h || !ptr || which < 0 || which > 2) return fail(AXONN_ERR_ARG, "bad argument");
-  const axonn_fc::Fused* f = which == 0 ? &h->fo : which == 1 ? &h->fi : &h->fw;
+  const axonn_fc::Fused* f = which == 0 ? &h->fo : which == 1 ? &h->fi
+                            : h->fd.epi.mode != axonn::kStore ? &h->fd : &h->fw;
   *ptr = f->epi.mode != axonn::kStore ? f->out.ptr : nullptr;
   return AXONN_OK;
 }
@@ -901,6 +971,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   const bool fI = h->fi.epi.mode != axonn::kStore;  // dI all-reduce fused into the dI GEMM
   const bool fW = h->fw.epi.mode != axonn::kStore;  // data-parallel dŴ all-reduce fused into the dW GEMM
   const bool fZ = h->fz.epi.mode == axonn::kScatter;  // RS_z fused into the dW GEMM
+  const bool fD = fZ && h->fd.epi.mode == axonn::kScatter;  // DP sum fused behind RS_z
   const size_t es = elem_size(dt);
   void* dst = fW ? h->fw.out.ptr : (rs && !fZ ? h->dwpart : dW_hat);
   const size_t S_el = static_cast<size_t>(g.what_len);
@@ -912,23 +983,41 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   };
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
   auto dW_gemm = [&]() -> axonn_status_t {
-    if (fZ)  // the previous fused RS_z must have released every rank's slots
-      CUDA_TRY(wait_xcall(st, h->ev_rsdone));
+    // the previous RS_z of this layer must be done with its source: the
+    // fused one's slots on every rank (released by its final Z barrier), or
+    // the NCCL one's read of dwpart (write-after-read race)
+    if (rs) CUDA_TRY(wait_xcall(st, h->ev_rsdone));
     return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
                     st, fW ? &h->fw.epi : (fZ ? &h->fz.epi : nullptr));
   };
   // line 14 (ORS, waited in grads_sync) and the per-layer data-parallel sum
   auto grad_comm = [&]() -> axonn_status_t {
-    if (rs && fZ) {
-      // fused RS_z, owner phase deferred on the Z stream (ORS): sum the Gz
-      // slots in rank order into this rank's Ŵ gradient slice
-      cudaStream_t zs = S.cstream[AX_Z];
+    cudaStream_t zs = S.cstream[AX_Z];
+    if (rs) {
       CUDA_TRY(cudaEventRecord(h->ev_rs, st));
       CUDA_TRY(cudaStreamWaitEvent(zs, h->ev_rs, 0));
+      // the previous data-parallel reduction of this layer is done with dŴ
+      // (NCCL) or with the DATA receive slots (fused: its final DATA barrier
+      // means every DATA owner finished reading them)
+      CUDA_TRY(wait_xcall(zs, h->ev_wdone));
+    }
+    if (rs && fZ) {
+      // fused RS_z, owner phase deferred on the Z stream (ORS): sum the Gz
+      // slots in rank order into this rank's Ŵ gradient slice, or — fused
+      // data-parallel sum — into the DATA owners' receive slots
       STATUS_TRY(fused_barrier(AX_Z, zs));  // every rank's scatter has landed
-      CUDA_TRY(axonn::sym_owner_reduce(&h->fz.recv, nullptr, h->fz.epi.slice, h->fz.epi.P,
-                                       h->fz.epi.me, S.num_sms, zs, dW_hat, nullptr,
-                                       h->fz.es == 4));
+      axonn::OwnerOut o;
+      if (fD) {
+        o.mode = axonn::kOwnScatter;
+        for (int q = 0; q < S.g[AX_D]; ++q) o.dst[q] = h->fd.epi.peer[q];
+        o.me2 = h->fd.epi.me;
+        o.slice2 = h->fd.epi.slice;
+      } else {
+        o.n_dst = 1;
+        o.dst[0] = reinterpret_cast<unsigned long long>(dW_hat);
+      }
+      CUDA_TRY(axonn::sym_owner_reduce(h->fz.recv.ptr, h->fz.epi.slice, h->fz.epi.P,
+                                       h->fz.es == 4, o, S.num_sms, zs));
       g_launches.fetch_add(1);
       STATUS_TRY(fused_barrier(AX_Z, zs));  // every owner is done with its slots
       CUDA_TRY(record_xcall(h->ev_rsdone, zs));
@@ -936,21 +1025,28 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
       CUDA_TRY(cudaEventRecord(h->ev_grad, zs));
       last = h->ev_grad;
     } else if (rs) {
-      CUDA_TRY(cudaEventRecord(h->ev_rs, st));
-      CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_Z], h->ev_rs, 0));
-      NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, gnt, ncclSum, S.axis_comm[AX_Z],
-                                 S.cstream[AX_Z]));
+      NCCL_TRY(ncclReduceScatter(h->dwpart, dW_hat, S_el, gnt, ncclSum, S.axis_comm[AX_Z], zs));
+      CUDA_TRY(record_xcall(h->ev_rsdone, zs));
       count_comm(1, S.g[AX_Z], S_el, gdt);
-      CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_Z]));
+      CUDA_TRY(cudaEventRecord(h->ev_grad, zs));
       last = h->ev_grad;
     }
     if (S.g[AX_D] > 1) {
-      CUDA_TRY(cudaEventRecord(h->ev_rs, rs ? S.cstream[AX_Z] : st));
-      CUDA_TRY(cudaStreamWaitEvent(S.cstream[AX_D], h->ev_rs, 0));
-      NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, gnt, ncclSum, S.axis_comm[AX_D],
-                             S.cstream[AX_D]));
+      cudaStream_t ds = S.cstream[AX_D];
+      CUDA_TRY(cudaEventRecord(h->ev_rs, rs ? zs : st));
+      CUDA_TRY(cudaStreamWaitEvent(ds, h->ev_rs, 0));
+      if (fD) {
+        // the DATA owner phase: barrier, sum the Gd slots, broadcast, barrier
+        STATUS_TRY(fused_post(h->fd, ds, 1));
+        if (dW_hat != h->fd.out.ptr)
+          CUDA_TRY(cudaMemcpyAsync(dW_hat, h->fd.out.ptr, S_el * h->fd.es,
+                                   cudaMemcpyDeviceToDevice, ds));
+      } else {
+        NCCL_TRY(ncclAllReduce(dW_hat, dW_hat, S_el, gnt, ncclSum, S.axis_comm[AX_D], ds));
+      }
       count_comm(4, S.g[AX_D], S_el, gdt);
-      CUDA_TRY(cudaEventRecord(h->ev_grad, S.cstream[AX_D]));
+      CUDA_TRY(record_xcall(h->ev_wdone, ds));
+      CUDA_TRY(cudaEventRecord(h->ev_grad, ds));
       last = h->ev_grad;
     }
     return AXONN_OK;
@@ -1042,7 +1138,7 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
     if (e) cudaEventDestroy(e);
   if (h->wbuf) cudaFree(h->wbuf);
   if (h->dwpart) cudaFree(h->dwpart);
-  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz}) {
+  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz, &h->fd}) {
     axonn::sym_free(&S.sym[f->axis], &f->out);
     axonn::sym_free(&S.sym[f->axis], &f->recv);
   }
@@ -1064,6 +1160,25 @@ axonn_status_t axonn_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, co
   if ((K && M && lda < a_cols) || (K && N && ldb < b_cols) || (M && ldc < N))
     return fail(AXONN_ERR_ARG, "leading dimension smaller than the row length");
   return run_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, as_stream(stream));
+}
+
+axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
+                                   const void* const* I_local, const void* const* W_hat,
+                                   const void* const* dO_local, void* const* O_local,
+                                   void* const* dI_local, void* const* dW_hat, int flags,
+                                   void* stream, int* paths) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  STATUS_TRY(check_grid_args(gx, gy, gz, gd));
+  if (!desc || !I_local || !W_hat || !dO_local || !O_local || !dI_local || !dW_hat)
+    return fail(AXONN_ERR_ARG, "NULL argument");
+  if (gx * gy * gz * gd > 64) return fail(AXONN_ERR_ARG, "loopback: at most 64 ranks");
+  if (gx > 8 || gy > 8 || gz > 8 || gd > 8)
+    return fail(AXONN_ERR_UNSUPPORTED, "loopback: fused collectives span at most 8 ranks per axis");
+  if (!valid_dtype(desc->dtype)) return fail(AXONN_ERR_ARG, "bad dtype");
+  STATUS_TRY(ensure_device());
+  const int g[4] = {gx, gy, gz, gd};
+  return axonn::loopback_step(desc, g, I_local, W_hat, dO_local, O_local, dI_local, dW_hat, flags,
+                              as_stream(stream), paths);
 }
 
 axonn_status_t axonn_profile_enable(int enabled) {

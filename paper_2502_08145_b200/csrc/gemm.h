@@ -14,7 +14,10 @@ namespace axonn {
 //   kScatter   plain NVLink stores of each 16-B vector into its owner rank's
 //              receive slot: owner o = flat index / slice, destination
 //              peer[o] + (me * slice + flat - o * slice) (fused reduce-scatter;
-//              needs ldc == N and slice % 8 == 0).
+//              needs ldc == N and slice % 8 == 0);
+//   kRedLocal  red.global.add of each 16-B bf16 vector at mc + offset: the
+//              single-GPU loopback's stand-in for kMcRed when the device
+//              has no multicast support (axonn_loopback_step).
 struct EpiTarget {
   int mode = 0;
   int P = 0, me = 0;
@@ -22,7 +25,7 @@ struct EpiTarget {
   unsigned long long mc = 0;
   unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
-enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2 };
+enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3 };
 
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 
@@ -31,6 +34,10 @@ enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, k
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
                         cudaStream_t stream, const EpiTarget* epi = nullptr, bool out_f32 = false);
+
+// The launch error behind the last GemmStatus::kLaunch on this thread (the
+// launch helpers consume cudaGetLastError()).
+cudaError_t gemm_last_launch_error();
 
 // fp32 SIMT FMA (test mode, no TF32): same op codes.
 GemmStatus gemm_f32_simt(int op, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

@@ -606,6 +606,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                 // fused 2-rank all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
                 ptx::multimem_red_add_bf16x8(
                     epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
+              } else if (epi.mode == kRedLocal) {
+                ptx::red_add_bf16x8(epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
               } else if (epi.mode == kScatter) {
                 // fused reduce-scatter: this 16-B vector goes to its owner's slot
                 const long long f = static_cast<long long>(grow) * N + gcol;
@@ -788,6 +790,8 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
+thread_local cudaError_t g_launch_error = cudaSuccess;
+
 // C[M][N] (bf16, ldc) = op(A) x op(B); see axonn_gemm in include/axonn.h.
 // AXONN_GEMM_VARIANT=single selects the 1-CTA kernel (kept for A/B timing);
 // the default is the CTA-pair kernel: 512x256 tiles for plain launches
@@ -840,7 +844,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode != kStore && (single || (N % unit) || (ldc % unit)))
     return GemmStatus::kBadAlignment;
   if (out_f32 && op != 2) return GemmStatus::kBadOp;  // fp32 output: the dW (TN) product only
-  if (out_f32 && epi.mode == kMcRed) return GemmStatus::kBadAlignment;  // red.add is bf16 here
+  if (out_f32 && (epi.mode == kMcRed || epi.mode == kRedLocal))
+    return GemmStatus::kBadAlignment;  // red.add is bf16 here
   if (epi.mode == kScatter && (ldc != N || epi.slice % unit || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   // MT=2's single accumulator serialises the epilogue with the next tile; on
@@ -878,7 +883,10 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
         : op == 1 ? launch_pair_mt<0, 0>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream)
                   : launch_pair_mt<1, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream);
   }
+  g_launch_error = e;
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;
 }
+
+cudaError_t gemm_last_launch_error() { return g_launch_error; }
 
 }  // namespace axonn

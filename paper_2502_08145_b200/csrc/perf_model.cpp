@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 
 namespace axonn {
@@ -114,15 +115,31 @@ int rank_configs(const std::vector<Layer>& layers, int G, int g_node,
     s.t.comm = s.t.ag_z + s.t.rs_z + s.t.ar_y + s.t.ar_x + s.t.ar_d;
     out->push_back(s);
   }
-  // Ascending t_comm; values equal to 1e-12 relative are ties broken
-  // lexicographically on (gx, gy, gz, gd) (R12).
-  std::stable_sort(out->begin(), out->end(), [](const Scored& a, const Scored& b2) {
-    const double tol = 1e-12 * std::max(std::fabs(a.t.comm), std::fabs(b2.t.comm));
-    if (std::fabs(a.t.comm - b2.t.comm) > tol) return a.t.comm < b2.t.comm;
-    const int ka[4] = {a.c.gx, a.c.gy, a.c.gz, a.c.gd};
-    const int kb[4] = {b2.c.gx, b2.c.gy, b2.c.gz, b2.c.gd};
+  // Ascending t_comm; ties broken lexicographically on (gx, gy, gz, gd) (R12).
+  // t_comm is first rounded to 12 significant digits, a canonical key, so
+  // sums that differ only by floating-point summation order compare equal
+  // and the comparison stays a strict weak ordering (a tolerance compare
+  // would not be transitive).
+  auto key = [](double t) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.11e", t);
+    return std::strtod(buf, nullptr);
+  };
+  std::vector<std::pair<double, size_t>> order(out->size());
+  for (size_t i = 0; i < out->size(); ++i) order[i] = {key((*out)[i].t.comm), i};
+  std::sort(order.begin(), order.end(), [&](const std::pair<double, size_t>& a,
+                                            const std::pair<double, size_t>& b2) {
+    if (a.first != b2.first) return a.first < b2.first;
+    const Config& x = (*out)[a.second].c;
+    const Config& y = (*out)[b2.second].c;
+    const int ka[4] = {x.gx, x.gy, x.gz, x.gd};
+    const int kb[4] = {y.gx, y.gy, y.gz, y.gd};
     return std::lexicographical_compare(ka, ka + 4, kb, kb + 4);
   });
+  std::vector<Scored> sorted;
+  sorted.reserve(out->size());
+  for (const auto& o : order) sorted.push_back((*out)[o.second]);
+  out->swap(sorted);
   return static_cast<int>(out->size());
 }
 

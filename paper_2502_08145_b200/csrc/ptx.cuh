@@ -302,6 +302,12 @@ __device__ __forceinline__ void multimem_red_add_bf16x8(uint64_t mc_addr, uint4 
                : "memory");
 }
 
+// Local (or peer) bf16x8 atomic add: the loopback's stand-in for multimem.red.
+__device__ __forceinline__ void red_add_bf16x8(uint64_t addr, uint4 v) {
+  asm volatile("red.relaxed.gpu.global.add.noftz.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(addr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {

@@ -60,17 +60,19 @@ __global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
   }
 }
 
-// Owner phase of the P-rank fused all-reduce: sum the P slots this rank
+// Owner phase of a P-rank fused reduction: sum the P slots this rank
 // received (fixed order src = 0..P-1, fp32, one RNE rounding to bf16) and
-// broadcast the result into every rank's output copy with multimem.st.  Every
-// element is reduced by exactly one rank, so all replicas hold the same bits.
-// F32 = false: 16-B units of 8 bf16, summed in fp32 in rank order and rounded
-// once (RNE); F32 = true: 4 fp32, summed in fp32 in rank order (fp32 gradient
-// reduction, reading R17).
+// send the result where `out` says (OwnerOut, sym.h): its own copy (+ the
+// peer's on 2-rank axes), every rank's copy through multimem.st, or the
+// owners of a second reduction axis (RS_z feeding the data-parallel sum).
+// Every element is reduced by exactly one rank, so all replicas hold the
+// same bits.  F32 = false: 16-B units of 8 bf16, summed in fp32 in rank order
+// and rounded once (RNE); F32 = true: 4 fp32, summed in fp32 in rank order
+// (fp32 gradient reduction, reading R17).
 template <bool F32>
 __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, int P,
-                               unsigned long long out_mc, uint4* __restrict__ out_local,
-                               uint4* __restrict__ out_peer) {
+                               const __grid_constant__ OwnerOut out) {
+  constexpr int UNIT = F32 ? 4 : 8;  // elements per 16-B unit
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n16;
        i += stride) {
@@ -98,14 +100,20 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, in
         o[q] = *reinterpret_cast<uint32_t*>(&h);
       }
     }
-    if (out_local) {  // reduce-scatter: the owner keeps its slice ...
-      out_local[i] = make_uint4(o[0], o[1], o[2], o[3]);
-      if (out_peer) out_peer[i] = make_uint4(o[0], o[1], o[2], o[3]);  // ... 2 ranks: and sends it
-    } else {
+    const uint4 r = make_uint4(o[0], o[1], o[2], o[3]);
+    if (out.mode == kOwnMc) {
       asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
-                       out_mc + static_cast<unsigned long long>(i) * 16),
+                       out.dst[0] + static_cast<unsigned long long>(i) * 16),
                    "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
                    : "memory");
+    } else if (out.mode == kOwnScatter) {
+      const long long f = i * UNIT;  // element index inside this owner's slice
+      const int ow = static_cast<int>(f / out.slice2);
+      const long long off = static_cast<long long>(out.me2) * out.slice2 + (f - ow * out.slice2);
+      *reinterpret_cast<uint4*>(out.dst[ow] + static_cast<unsigned long long>(off) * (16 / UNIT)) = r;
+    } else {
+      for (int d = 0; d < out.n_dst; ++d)
+        reinterpret_cast<uint4*>(out.dst[d])[i] = r;
     }
   }
   asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -172,12 +180,8 @@ void sym_axis_destroy(SymAxis* a) {
   a->impl = nullptr;
 }
 
-bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why) {
+bool sym_mem_alloc(size_t bytes, SymBuf* out, std::string* why) {
   *out = SymBuf();
-  if (!a->impl) {
-    *why = "axis has no symmetric-memory communicator";
-    return false;
-  }
   static const bool fail_test = [] {  // test hook: exercise the NCCL fallback
     const char* v = std::getenv("AXONN_SYM_ALLOC_FAIL");
     return v && std::atoi(v) != 0;
@@ -193,43 +197,62 @@ bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why) {
     *why = std::string("ncclMemAlloc: ") + ncclGetErrorString(r);
     return false;
   }
+  out->ptr = p;
+  out->bytes = bytes;
+  return true;
+}
+
+bool sym_register(SymAxis* a, SymBuf* b, std::string* why) {
+  if (!a->impl || !b->ptr) {
+    *why = !a->impl ? "axis has no symmetric-memory communicator" : "nothing allocated";
+    return false;
+  }
   ncclWindow_t win = nullptr;
-  r = ncclCommWindowRegister(a->impl->comm, p, bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
+  ncclResult_t r = ncclCommWindowRegister(a->impl->comm, b->ptr, b->bytes, &win,
+                                          NCCL_WIN_COLL_SYMMETRIC);
   if (r != ncclSuccess) {
-    ncclMemFree(p);
     *why = std::string("ncclCommWindowRegister: ") + ncclGetErrorString(r);
     return false;
   }
+  b->win = win;
   void** dptr = nullptr;
   void* host[2] = {nullptr, nullptr};
-  if (cudaMalloc(&dptr, 2 * sizeof(void*)) != cudaSuccess) {
-    *why = "cudaMalloc";
-    return false;
+  cudaError_t e = cudaMalloc(&dptr, 2 * sizeof(void*));
+  if (e == cudaSuccess) {
+    k_mc_ptr<<<1, 1>>>(win, a->impl->dev, dptr);
+    e = cudaMemcpy(host, dptr, sizeof host, cudaMemcpyDeviceToHost);
+    cudaFree(dptr);
   }
-  k_mc_ptr<<<1, 1>>>(win, a->impl->dev, dptr);
-  cudaError_t e = cudaMemcpy(host, dptr, sizeof host, cudaMemcpyDeviceToHost);
-  cudaFree(dptr);
   // host[1] is this rank's slot in NCCL's flat LSA mapping: another virtual
-  // address of the same physical pages as p.
+  // address of the same physical pages as ptr.  The window stays registered
+  // on failure (sym_free deregisters it) so every rank's calls stay matched.
   if (e != cudaSuccess || host[0] == nullptr) {
-    ncclCommWindowDeregister(a->impl->comm, win);
-    ncclMemFree(p);
     char buf[160];
     std::snprintf(buf, sizeof buf, "multicast address of the window unavailable (%s, mc=%p)",
                   cudaGetErrorString(e), host[0]);
     *why = buf;
     return false;
   }
-  out->ptr = p;
-  out->mc = host[0];
-  out->bytes = bytes;
-  out->win = win;
+  b->mc = host[0];
+  return true;
+}
+
+bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why) {
+  if (!a->impl) {
+    *why = "axis has no symmetric-memory communicator";
+    return false;
+  }
+  if (!sym_mem_alloc(bytes, out, why)) return false;
+  if (!sym_register(a, out, why)) {
+    sym_free(a, out);
+    return false;
+  }
   return true;
 }
 
 void sym_free(SymAxis* a, SymBuf* b) {
   if (!b->ptr) return;
-  if (a->impl) ncclCommWindowDeregister(a->impl->comm, static_cast<ncclWindow_t>(b->win));
+  if (a->impl && b->win) ncclCommWindowDeregister(a->impl->comm, static_cast<ncclWindow_t>(b->win));
   ncclMemFree(b->ptr);
   *b = SymBuf();
 }
@@ -267,23 +290,59 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
   return cudaDeviceSynchronize();
 }
 
-cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
-                             int me, int num_sms, cudaStream_t st, void* out_local,
-                             void* out_peer, bool f32) {
+cudaError_t sym_owner_reduce(const void* recv, long long slice, int P, bool f32,
+                             const OwnerOut& out, int num_sms, cudaStream_t st) {
   const int es = f32 ? 4 : 2;
+  if (P < 1 || P > 8 || (slice * es) % 16 || out.n_dst < 0 || out.n_dst > 8 ||
+      (out.mode == kOwnScatter && (out.slice2 <= 0 || (out.slice2 * es) % 16)))
+    return cudaErrorInvalidValue;
   const long long n16 = slice * es / 16;
   long long blocks = (n16 + 255) / 256;
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
   if (blocks < 1) blocks = 1;
-  const unsigned long long mc =
-      out_local ? 0ULL
-                : reinterpret_cast<unsigned long long>(out->mc) +
-                      static_cast<unsigned long long>(me) * slice * es;
   auto kern = f32 ? k_owner_reduce<true> : k_owner_reduce<false>;
-  kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-      reinterpret_cast<const uint4*>(recv->ptr), n16, P, mc, static_cast<uint4*>(out_local),
-      static_cast<uint4*>(out_peer));
+  kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const uint4*>(recv), n16, P,
+                                                      out);
   return cudaGetLastError();
+}
+
+cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* dst,
+                            cudaStream_t st) {
+  for (int q = 0; q < P; ++q) {
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + q * bytes, src[q], bytes,
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k) {
+  const int64_t n = rows * cols;
+  const int unit = 16 / es;  // elements per 16-B epilogue unit
+  // not fused: a 1-rank axis, an empty output, rows not a whole number of
+  // 16-B units, or an empty product (K == 0 writes zeros; nothing to scatter)
+  if (P < 2 || n <= 0 || cols % unit || kdim <= 0) return kStore;
+  // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
+  if (es == 2 && P == 2 && kdim >= red_min_k) return kMcRed;
+  if (n % (static_cast<int64_t>(unit) * P)) return kStore;
+  return kScatter;
+}
+
+EpiTarget epi_red(unsigned long long mc) {
+  EpiTarget t;
+  t.mode = kMcRed;
+  t.mc = mc;
+  return t;
+}
+
+EpiTarget epi_scatter(int P, int me, long long slice, const unsigned long long* peer) {
+  EpiTarget t;
+  t.mode = kScatter;
+  t.P = P;
+  t.me = me;
+  t.slice = slice;
+  for (int q = 0; q < P && q < 8; ++q) t.peer[q] = peer[q];
+  return t;
 }
 
 cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* dst, int num_sms,

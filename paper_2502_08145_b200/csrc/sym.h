@@ -1,11 +1,14 @@
-// sym.h — symmetric NVLink memory for the fused GEMM + all-reduce (see sym.cu).
+// sym.h — symmetric NVLink memory for the fused GEMM + collective paths (see sym.cu).
 #pragma once
 
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <cstddef>
+#include <cstdint>
 #include <string>
+
+#include "gemm.h"
 
 namespace axonn {
 
@@ -18,36 +21,76 @@ struct SymAxis {
 
 struct SymBuf {
   void* ptr = nullptr;  // this rank's copy (device pointer)
-  void* mc = nullptr;   // multicast address: a multimem.red lands in every rank's copy
+  void* mc = nullptr;   // multicast address: a multimem.red / .st lands in every rank's copy
   size_t bytes = 0;
-  void* win = nullptr;  // ncclWindow_t
+  void* win = nullptr;  // ncclWindow_t (null until sym_register)
 };
 
 bool sym_axis_init(ncclComm_t comm, SymAxis* out, std::string* why);
 void sym_axis_destroy(SymAxis* a);
+// Two phases, so that every rank makes the same sequence of collective calls
+// even when a local allocation fails (the caller agrees on the local results
+// before any registration):
+//   sym_mem_alloc  local: ncclMemAlloc of `bytes` rounded up to 2 MiB;
+//   sym_register   collective over the axis: window registration + the
+//                  window's multicast address.
+bool sym_mem_alloc(size_t bytes, SymBuf* out, std::string* why);
+bool sym_register(SymAxis* a, SymBuf* b, std::string* why);
+// Both phases (diagnostics only: the probe allocates on every rank alike).
 bool sym_alloc(SymAxis* a, size_t bytes, SymBuf* out, std::string* why);
 void sym_free(SymAxis* a, SymBuf* b);
-// Diagnostics: device address of `peer`'s copy; NVLink primitive throughput
-// probe over the whole buffer (mode 0 multimem.red bf16, 1 multimem.st,
-// 2 plain store to peer, 3 multimem.ld_reduce, 4 local store).
+// Device address of `peer`'s copy of a registered buffer (LSA), or null.
 void* sym_peer_ptr(SymBuf* b, int peer);
+// NVLink primitive throughput probe over the whole buffer (mode 0
+// multimem.red bf16, 1 multimem.st, 2 plain store to peer, 3
+// multimem.ld_reduce, 4 local store).
 cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms);
-// Owner phase of the P-rank fused all-reduce / reduce-scatter (see sym.cu):
-// recv holds P slots of `slice` elements (bf16, or fp32 when f32); the sum
-// goes to every rank's out[me*slice ...] (multicast), or to out_local when it
-// is non-null (and also to out_peer with plain NVLink stores when that is
-// non-null: 2-rank axes).
-cudaError_t sym_owner_reduce(const SymBuf* recv, const SymBuf* out, long long slice, int P,
-                             int me, int num_sms, cudaStream_t st, void* out_local = nullptr,
-                             void* out_peer = nullptr, bool f32 = false);
+
+// Where the owner phase of a fused reduction sends the reduced 16-B units of
+// its slice (unit u covers elements [u*U, u*U+U), U = 16 / element bytes):
+//   kOwnPlain    plain stores to dst[0 .. n_dst) + 16u (own copy, and the
+//                peer's copy on 2-rank axes);
+//   kOwnMc       multimem.st at dst[0] + 16u (every rank's copy, NVLS);
+//   kOwnScatter  the reduced slice is itself reduced over a second axis
+//                (RS_z followed by the data-parallel sum):
+//                element f of the slice goes to its owner o = f / slice2 on
+//                that axis, at dst[o] + (me2*slice2 + f - o*slice2) * es —
+//                the same addressing as the GEMM's kScatter epilogue.
+enum OwnMode { kOwnPlain = 0, kOwnMc = 1, kOwnScatter = 2 };
+struct OwnerOut {
+  int mode = kOwnPlain;
+  int n_dst = 0;
+  unsigned long long dst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int me2 = 0;
+  long long slice2 = 0;
+};
+// Owner phase: sum the P slots of `slice` elements in `recv` (bf16, or fp32
+// when f32) in rank order 0..P-1 in fp32, round once (bf16), write per `out`.
+cudaError_t sym_owner_reduce(const void* recv, long long slice, int P, bool f32,
+                             const OwnerOut& out, int num_sms, cudaStream_t st);
 // All-gather pull on the SMs: dst = src[0] | src[1] | ... | src[P-1], each
 // `bytes` long (bytes % 16 == 0; src are LSA peer addresses or local).
 cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* dst, int num_sms,
+                            cudaStream_t st);
+// All-gather on the copy engines (no SMs): one cudaMemcpyAsync per rank's
+// slice, in z order: dst[q*bytes ...] = src[q].
+cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* dst,
                             cudaStream_t st);
 // One-CTA cross-rank barrier on `st` (system-scope release/acquire).  Each
 // `index` (0 or 1) is its own barrier sequence: every rank must issue the
 // barriers of one index in the same order, and all barriers of one index must
 // be issued on one stream (the epoch state is not safe under concurrency).
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0);
+
+// Fused-reduction plan shared by the multi-GPU path (axonn.cpp) and the
+// single-GPU loopback (loopback.cpp): the epilogue mode of a rows x cols
+// output of a GEMM with contraction length kdim reduced over P ranks with
+// es-byte elements.  kStore means "not fused" (NCCL, or no reduction when
+// P == 1).  2-rank bf16 axes use multimem.red when kdim >= red_min_k.
+int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k);
+// Epilogue targets: multimem.red into `mc`; scatter of 16-B units to the
+// owners' receive slots peer[0..P) (owner o = flat / slice).
+EpiTarget epi_red(unsigned long long mc);
+EpiTarget epi_scatter(int P, int me, long long slice, const unsigned long long* peer);
 
 }  // namespace axonn

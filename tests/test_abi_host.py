@@ -90,7 +90,7 @@ def test_grid_select_matches_oracle(G, g_node, h, phase, gd):
 
 @pytest.mark.parametrize("G,gd", [(8, 0), (16, 2), (64, 0)])
 def test_grid_select_mp_matches_oracle(G, gd):
-    layers = pm.gpt_block(6144, 16384, "fwd")
+    layers = pm.gpt_block(6144, 16384, "A")
     tb = _table(8)
     want = pm.rank_configs(layers, G, 8, tb, 25e9, b=2, fixed_gd=gd, b_grad=4)
     got = ax.axonn_grid_select([(L.m, L.k, L.n, L.transposed) for L in layers], G, 8, tb,

@@ -151,9 +151,38 @@ def test_fp32_gradients_shift_the_ranking_toward_tensor_parallelism():
     # doubling only the gradient bytes makes Z/DATA (whose cost is all
     # gradient for DATA, half for Z) relatively dearer: the all-DATA config
     # never improves its rank
-    layers = pm.gpt_block(4096, 16384, "fwd")
+    layers = pm.gpt_block(4096, 16384, "A")
     tb = pm.uniform_table(8, GB)
     r2 = [c for c, _ in pm.rank_configs(layers, 8, 8, tb, GB, b=2)]
     r4 = [c for c, _ in pm.rank_configs(layers, 8, 8, tb, GB, b=2, b_grad=4)]
     assert sorted(r2) == sorted(r4)
     assert r4.index((1, 1, 1, 8)) >= r2.index((1, 1, 1, 8))
+
+
+def test_gpt_block_rejects_unknown_phase():
+    # reading R2b names exactly two phases; anything else is a caller error,
+    # not a silent phase B
+    with pytest.raises(ValueError, match="phase"):
+        pm.gpt_block(4096, 16384, "fwd")
+    assert [L.transposed for L in pm.gpt_block(64, 8, "B")] == [True, False, True, False]
+
+
+@pytest.mark.parametrize("cfg,g_node,want", [
+    # Case 1 while prod_{j<=i} G_j <= g_node, else Eq. 7: beta_inter / min(g_node, prod_{j<i} G_j)
+    ((2, 2, 2, 2), 4, ("T12", "T22", "B/4", "B/4")),
+    ((8, 1, 1, 1), 4, ("B/1", "inf", "inf", "inf")),
+    ((1, 2, 4, 2), 2, ("inf", "T12", "B/2", "B/2")),
+    ((2, 1, 1, 8), 1, ("B/1", "inf", "inf", "B/1")),
+    ((4, 2, 2, 1), 8, ("T14", "T42", "B/8", "inf")),
+    ((2, 4, 2, 2), 8, ("T12", "T24", "B/8", "B/8")),
+    ((1, 1, 4, 4), 2, ("inf", "inf", "B/1", "B/2")),
+])
+def test_eq7_hand_computed_case2_betas(cfg, g_node, want):
+    """Eq. 7 on grids that span nodes, each beta worked by
+    hand from the hierarchy products (X, Y, Z, DATA innermost first)."""
+    B = 100e9
+    T = {(1, 2): 510e9, (2, 2): 470e9, (1, 4): 630e9, (4, 2): 300e9, (2, 4): 280e9,
+         (1, 8): 700e9}
+    hand = {"inf": inf, "T12": T[(1, 2)], "T22": T[(2, 2)], "T14": T[(1, 4)], "T42": T[(4, 2)],
+            "T24": T[(2, 4)], "B/1": B, "B/2": B / 2, "B/4": B / 4, "B/8": B / 8}
+    assert pm.effective_bandwidths(cfg, g_node, T, B) == tuple(hand[w] for w in want)
