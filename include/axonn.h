@@ -259,7 +259,9 @@ enum {
   AXONN_LB_RED_ALWAYS = 1,   /* 2-rank bf16 axes: multimem.red at any K          */
   AXONN_LB_RED_NEVER = 2,    /* never multimem.red: scatter + owner phase        */
   AXONN_LB_GATHER_PULL = 4,  /* AG_z by the SM pull kernel (else copy engines)   */
-  AXONN_LB_EMULATE_MC = 8    /* no multicast object: red.global.add / plain st   */
+  AXONN_LB_EMULATE_MC = 8,   /* no multicast object: red.global.add / plain st   */
+  AXONN_LB_NO_EXCHANGE = 16  /* 2-rank axes below the red threshold: scatter +
+                                owner phase instead of the exchange of partials */
 };
 enum {
   AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,
@@ -268,7 +270,9 @@ enum {
   AXONN_LB_PATH_DP_RED = 32, AXONN_LB_PATH_DP_SCATTER = 64,
   AXONN_LB_PATH_DP_AFTER_RS = 128,
   AXONN_LB_PATH_GATHER_COPY = 256, AXONN_LB_PATH_GATHER_PULL = 512,
-  AXONN_LB_PATH_MULTICAST = 1024   /* a real one-device multicast object was used */
+  AXONN_LB_PATH_MULTICAST = 1024,  /* a real one-device multicast object was used */
+  AXONN_LB_PATH_FWD_EXCHANGE = 2048, AXONN_LB_PATH_BWD_EXCHANGE = 4096,
+  AXONN_LB_PATH_DP_EXCHANGE = 8192
 };
 axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
                                    const void* const* I_local, const void* const* W_hat,

@@ -328,7 +328,9 @@ struct axonn_fc {
     size_t elems = 0;
     void* out_peer = nullptr;  // 2-rank scatter mode: the peer's copy of our slice
     axonn::SymBuf out;    // every rank's result (handle-owned output buffer)
-    axonn::SymBuf recv;   // P-rank scatter mode: P slots of elems / P
+    axonn::SymBuf recv;   // P-rank scatter mode: P slots of elems / P; exchange: P slots of elems
+    axonn::SymBuf recv2;  // exchange mode: the second receive buffer (device-side parity)
+    int* par = nullptr;   // exchange mode: parity counter, advanced by the post barrier
     axonn::EpiTarget epi;
   };
   Fused fo;   // O   over the forward axis      (Alg. 1 line 4 fused into line 3)
@@ -384,12 +386,18 @@ void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_
   f->epi = axonn::EpiTarget();
   if (!S.sym[axis].impl) return;
   const int mode = axonn::fused_mode(S.g[axis], es, rows, cols, kdim,
-                                     env_int("AXONN_RED_MIN_K", 8192));
+                                     env_int("AXONN_RED_MIN_K", 8192),
+                                     env_int("AXONN_EXCHANGE", 1) != 0);
   if (mode == axonn::kStore) return;
   f->elems = static_cast<size_t>(rows * cols);
   f->epi.mode = mode;  // targets are bound after registration (fused_bind)
   reqs->push_back({axis, f->elems * es, &f->out});
   if (mode == axonn::kScatter) reqs->push_back({axis, f->elems * es, &f->recv});
+  if (mode == axonn::kExchange) {
+    const int P = S.g[axis];
+    reqs->push_back({axis, f->elems * es * P, &f->recv});
+    reqs->push_back({axis, f->elems * es * P, &f->recv2});
+  }
 }
 
 // After registration: the epilogue targets (multicast address, or every
@@ -408,6 +416,22 @@ bool fused_bind(axonn_fc::Fused* f, std::string* why) {
       *why = "peer address of the receive window unavailable";
       return false;
     }
+  }
+  if (f->epi.mode == axonn::kExchange) {
+    unsigned long long alt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < P; ++q) {
+      alt[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv2, q));
+      if (!alt[q]) {
+        *why = "peer address of the receive window unavailable";
+        return false;
+      }
+    }
+    if (cudaMalloc(&f->par, sizeof(int)) != cudaSuccess || cudaMemset(f->par, 0, sizeof(int)) != cudaSuccess) {
+      *why = "cudaMalloc of the exchange parity counter failed";
+      return false;
+    }
+    f->epi = axonn::epi_exchange(P, me, static_cast<long long>(f->elems), peer, alt, f->par);
+    return true;
   }
   f->epi = axonn::epi_scatter(P, me, static_cast<long long>(f->elems) / P, peer);
   if (P == 2) {  // the owner sends its reduced slice to the peer with plain stores
@@ -445,6 +469,9 @@ axonn_status_t fused_barrier(int axis, cudaStream_t st, int index = 0);
 void fused_reset(axonn_fc::Fused* f) {
   axonn::sym_free(&S.sym[f->axis], &f->out);
   axonn::sym_free(&S.sym[f->axis], &f->recv);
+  axonn::sym_free(&S.sym[f->axis], &f->recv2);
+  if (f->par) cudaFree(f->par);
+  f->par = nullptr;
   f->epi = axonn::EpiTarget();
   f->out_peer = nullptr;
   f->elems = 0;
@@ -474,6 +501,20 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
 }
 
 axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
+  if (f.epi.mode == axonn::kExchange) {
+    // every rank's whole partial has landed in our slots (the barrier also
+    // advances the parity counter); the sum is local, in slot order, so all
+    // ranks hold the same bits and nothing crosses NVLink after the barrier
+    CUDA_TRY(axonn::sym_barrier(&S.sym[f.axis], st, index, f.par));
+    g_launches.fetch_add(1);
+    axonn::OwnerOut o;
+    o.n_dst = 1;
+    o.dst[0] = reinterpret_cast<unsigned long long>(f.out.ptr);
+    CUDA_TRY(axonn::sym_owner_reduce(f.recv.ptr, static_cast<long long>(f.elems), f.epi.P,
+                                     f.es == 4, o, S.num_sms, st, f.par, f.recv2.ptr));
+    g_launches.fetch_add(1);
+    return AXONN_OK;
+  }
   STATUS_TRY(fused_barrier(f.axis, st, index));  // every rank's epilogue writes have landed
   if (f.epi.mode == axonn::kScatter) {
     CUDA_TRY(axonn::sym_owner_reduce(f.recv.ptr, f.epi.slice, f.epi.P, f.es == 4, owner_out(f),
@@ -1138,10 +1179,7 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
     if (e) cudaEventDestroy(e);
   if (h->wbuf) cudaFree(h->wbuf);
   if (h->dwpart) cudaFree(h->dwpart);
-  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz, &h->fd}) {
-    axonn::sym_free(&S.sym[f->axis], &f->out);
-    axonn::sym_free(&S.sym[f->axis], &f->recv);
-  }
+  for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz, &h->fd}) fused_reset(f);
   axonn::sym_free(&S.sym[AX_Z], &h->wstage);
   delete h;
   return AXONN_OK;

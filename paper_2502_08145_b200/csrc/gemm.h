@@ -15,6 +15,12 @@ namespace axonn {
 //              receive slot: owner o = flat index / slice, destination
 //              peer[o] + (me * slice + flat - o * slice) (fused reduce-scatter;
 //              needs ldc == N and slice % 8 == 0);
+//   kExchange  every rank's whole partial to every rank of the axis: plain
+//              stores of each 16-B vector to slot `me` of each rank's receive
+//              buffer, peer[q] + (me * slice + flat) (slice = M*N, ldc == N);
+//              the post phase is a local sum of the P slots (2-rank axes).
+//              With `par` set, the kernel reads *par and targets peer_alt
+//              instead when it is odd (device-side double buffering).
 //   kRedLocal  red.global.add of each 16-B bf16 vector at mc + offset: the
 //              single-GPU loopback's stand-in for kMcRed when the device
 //              has no multicast support (axonn_loopback_step).
@@ -24,8 +30,10 @@ struct EpiTarget {
   long long slice = 0;
   unsigned long long mc = 0;
   unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long peer_alt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int* par = nullptr;
 };
-enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3 };
+enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4 };
 
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 

@@ -519,6 +519,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
     const bool vec_ok =
         ((ldc * ELEM) % 16 == 0) && ((reinterpret_cast<uintptr_t>(Cv) & 15) == 0);
     uint8_t* stage_base = sEpi + ew * (2 * 32 * 64 * 2);
+    // kExchange double buffering: the receive buffers of this call (parity
+    // counter written in stream order by the previous call's barrier kernel)
+    const unsigned long long* xbase =
+        (epi.mode == kExchange && epi.par && (*reinterpret_cast<const volatile int*>(epi.par) & 1))
+            ? epi.peer_alt
+            : epi.peer;
     int nstore = 0;  // TMA stores issued by this warp (alternate staging boxes)
     for (int seq = 0;; ++seq) {
       const int t = consume_tile(seq, false);
@@ -606,6 +612,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                 // fused 2-rank all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
                 ptx::multimem_red_add_bf16x8(
                     epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
+              } else if (epi.mode == kExchange) {
+                // all-reduce by exchange: this 16-B vector to slot `me` of every rank
+                const long long f = static_cast<long long>(grow) * N + gcol;
+                const uint64_t off =
+                    static_cast<uint64_t>(static_cast<long long>(epi.me) * epi.slice + f) * ELEM;
+                for (int q = 0; q < epi.P; ++q) *reinterpret_cast<uint4*>(xbase[q] + off) = w;
               } else if (epi.mode == kRedLocal) {
                 ptx::red_add_bf16x8(epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
               } else if (epi.mode == kScatter) {
@@ -847,6 +859,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (out_f32 && (epi.mode == kMcRed || epi.mode == kRedLocal))
     return GemmStatus::kBadAlignment;  // red.add is bf16 here
   if (epi.mode == kScatter && (ldc != N || epi.slice % unit || epi.P < 1 || epi.P > 8))
+    return GemmStatus::kBadAlignment;
+  if (epi.mode == kExchange && (ldc != N || epi.slice != M * N || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   // MT=2's single accumulator serialises the epilogue with the next tile; on
   // short K loops that costs more than its lower L2/DRAM traffic saves

@@ -263,6 +263,9 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   if (const char* v = std::getenv("AXONN_RED_MIN_K")) red_min_k = std::atoi(v);
   if (flags & AXONN_LB_RED_ALWAYS) red_min_k = 0;
   if (flags & AXONN_LB_RED_NEVER) red_min_k = INT_MAX;
+  bool exchange2 = true;
+  if (const char* v = std::getenv("AXONN_EXCHANGE")) exchange2 = std::atoi(v) != 0;
+  if (flags & AXONN_LB_NO_EXCHANGE) exchange2 = false;
   auto members = [&](int r, int axis) {
     std::vector<int> m(g[axis]);
     axonn_group_members(r, g[0], g[1], g[2], g[3], axis, m.data());
@@ -280,7 +283,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     op->es = es;
     op->elems = rows * cols;
     if (op->P == 1) return AXONN_OK;
-    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k);
+    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2);
     if (op->mode == kStore) {
       char buf[200];
       std::snprintf(buf, sizeof buf,
@@ -331,11 +334,13 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
         }
       }
     }
-    if (op->mode == kScatter) {
+    if (op->mode == kScatter || op->mode == kExchange) {
+      // scatter: P slots of elems / P; exchange: P slots of elems (whole partials)
+      const int64_t rbytes = op->elems * op->es * (op->mode == kExchange ? op->P : 1);
       op->recv.resize(G);
       op->out.resize(G, nullptr);
       for (int r = 0; r < G; ++r) {
-        op->recv[r] = static_cast<char*>(pool.get(op->elems * op->es));
+        op->recv[r] = static_cast<char*>(pool.get(rbytes));
         if (op->P == 2) op->out[r] = static_cast<char*>(pool.get(op->elems * op->es));
         if (!op->recv[r] || (op->P == 2 && !op->out[r]))
           return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
@@ -365,10 +370,11 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       if (!real_mc) t.mode = kRedLocal;
       return t;
     }
-    if (op.mode == kScatter) {
+    if (op.mode == kScatter || op.mode == kExchange) {
       const std::vector<int> mem = members(r, op.axis);
       unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int q = 0; q < op.P; ++q) peer[q] = reinterpret_cast<unsigned long long>(op.recv[mem[q]]);
+      if (op.mode == kExchange) return epi_exchange(op.P, cc[r][op.axis], op.elems, peer, nullptr, nullptr);
       return epi_scatter(op.P, cc[r][op.axis], op.elems / op.P, peer);
     }
     return EpiTarget();
@@ -401,6 +407,18 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   };
   // every rank's owner phase (scatter mode)
   auto owner_phase = [&](const LbOp& op) -> axonn_status_t {
+    if (op.mode == kExchange) {  // every rank sums its own P slots locally
+      for (int r = 0; r < G; ++r) {
+        OwnerOut o;
+        o.n_dst = 1;
+        o.dst[0] = reinterpret_cast<unsigned long long>(op.out[r]);
+        if (sym_owner_reduce(op.recv[r], op.elems, op.P, op.es == 4, o, rt_num_sms(), st) !=
+            cudaSuccess)
+          return rt_fail(AXONN_ERR_CUDA, "loopback: exchange sum launch failed");
+        rt_count_launch();
+      }
+      return AXONN_OK;
+    }
     if (op.mode != kScatter) return AXONN_OK;
     for (int r = 0; r < G; ++r) {
       if (sym_owner_reduce(op.recv[r], op.elems / op.P, op.P, op.es == 4, owner_out(op, r),
@@ -412,7 +430,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   };
   // the reduced result of rank r -> its caller buffer
   auto deliver = [&](const LbOp& op, int r, void* dst) -> axonn_status_t {
-    const char* src = (op.mode == kScatter && op.P == 2) ? op.out[r] : uc_of(op, r);
+    const char* src = ((op.mode == kScatter || op.mode == kExchange) && op.P == 2) ? op.out[r]
+                                                                                    : uc_of(op, r);
     if (op.elems &&
         cudaMemcpyAsync(dst, src, op.elems * op.es, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return rt_fail(AXONN_ERR_CUDA, "loopback: copy failed");
@@ -457,7 +476,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   }
   if ((s = owner_phase(fo)) != AXONN_OK) return s;
   if (fo.mode != kStore) {
-    p |= fo.mode == kMcRed ? AXONN_LB_PATH_FWD_RED : AXONN_LB_PATH_FWD_SCATTER;
+    p |= fo.mode == kMcRed ? AXONN_LB_PATH_FWD_RED
+         : fo.mode == kExchange ? AXONN_LB_PATH_FWD_EXCHANGE : AXONN_LB_PATH_FWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fo, r, O[r])) != AXONN_OK) return s;
   }
@@ -473,7 +493,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   }
   if ((s = owner_phase(fi)) != AXONN_OK) return s;
   if (fi.mode != kStore) {
-    p |= fi.mode == kMcRed ? AXONN_LB_PATH_BWD_RED : AXONN_LB_PATH_BWD_SCATTER;
+    p |= fi.mode == kMcRed ? AXONN_LB_PATH_BWD_RED
+         : fi.mode == kExchange ? AXONN_LB_PATH_BWD_EXCHANGE : AXONN_LB_PATH_BWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fi, r, dI[r])) != AXONN_OK) return s;
   }
@@ -520,7 +541,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   // ------------------------------------------------ data-parallel sum (Eq. 5)
   if (fw.mode != kStore) {
     if ((s = owner_phase(fw)) != AXONN_OK) return s;
-    p |= fw.mode == kMcRed ? AXONN_LB_PATH_DP_RED : AXONN_LB_PATH_DP_SCATTER;
+    p |= fw.mode == kMcRed ? AXONN_LB_PATH_DP_RED
+         : fw.mode == kExchange ? AXONN_LB_PATH_DP_EXCHANGE : AXONN_LB_PATH_DP_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fw, r, dW[r])) != AXONN_OK) return s;
   }

@@ -70,9 +70,13 @@ __global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
 // and rounded once (RNE); F32 = true: 4 fp32, summed in fp32 in rank order
 // (fp32 gradient reduction, reading R17).
 template <bool F32>
-__global__ void k_owner_reduce(const uint4* __restrict__ recv, long long n16, int P,
+__global__ void k_owner_reduce(const uint4* __restrict__ recv0, const uint4* __restrict__ recv1,
+                               const int* __restrict__ par, long long n16, int P,
                                const __grid_constant__ OwnerOut out) {
   constexpr int UNIT = F32 ? 4 : 8;  // elements per 16-B unit
+  // kExchange double buffering: the barrier before this kernel advanced the
+  // parity counter past the value the producing GEMM read
+  const uint4* __restrict__ recv = (par && ((*par - 1) & 1)) ? recv1 : recv0;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n16;
        i += stride) {
@@ -136,9 +140,11 @@ __global__ void k_gather_pull(PullSrc src, int P, long long n16, uint4* __restri
   }
 }
 
-__global__ void k_barrier(ncclDevComm dc, uint32_t index) {
+__global__ void k_barrier(ncclDevComm dc, uint32_t index, int* ctr) {
   ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), index);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  // kExchange parity: the next call's epilogue targets the other buffers
+  if (ctr && threadIdx.x == 0) *ctr += 1;
 }
 
 }  // namespace
@@ -291,7 +297,8 @@ cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int i
 }
 
 cudaError_t sym_owner_reduce(const void* recv, long long slice, int P, bool f32,
-                             const OwnerOut& out, int num_sms, cudaStream_t st) {
+                             const OwnerOut& out, int num_sms, cudaStream_t st, const int* par,
+                             const void* recv_alt) {
   const int es = f32 ? 4 : 2;
   if (P < 1 || P > 8 || (slice * es) % 16 || out.n_dst < 0 || out.n_dst > 8 ||
       (out.mode == kOwnScatter && (out.slice2 <= 0 || (out.slice2 * es) % 16)))
@@ -301,8 +308,9 @@ cudaError_t sym_owner_reduce(const void* recv, long long slice, int P, bool f32,
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
   if (blocks < 1) blocks = 1;
   auto kern = f32 ? k_owner_reduce<true> : k_owner_reduce<false>;
-  kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const uint4*>(recv), n16, P,
-                                                      out);
+  kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(recv), reinterpret_cast<const uint4*>(recv_alt ? recv_alt : recv),
+      par, n16, P, out);
   return cudaGetLastError();
 }
 
@@ -316,7 +324,8 @@ cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* d
   return cudaSuccess;
 }
 
-int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k) {
+int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
+               bool exchange2) {
   const int64_t n = rows * cols;
   const int unit = 16 / es;  // elements per 16-B epilogue unit
   // not fused: a 1-rank axis, an empty output, rows not a whole number of
@@ -324,8 +333,25 @@ int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_
   if (P < 2 || n <= 0 || cols % unit || kdim <= 0) return kStore;
   // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
   if (es == 2 && P == 2 && kdim >= red_min_k) return kMcRed;
+  // 2-rank axes: exchange whole partials, then sum locally (no owner broadcast)
+  if (P == 2 && exchange2) return kExchange;
   if (n % (static_cast<int64_t>(unit) * P)) return kStore;
   return kScatter;
+}
+
+EpiTarget epi_exchange(int P, int me, long long n, const unsigned long long* recv,
+                       const unsigned long long* recv_alt, const int* par) {
+  EpiTarget t;
+  t.mode = kExchange;
+  t.P = P;
+  t.me = me;
+  t.slice = n;
+  for (int q = 0; q < P && q < 8; ++q) {
+    t.peer[q] = recv[q];
+    t.peer_alt[q] = recv_alt ? recv_alt[q] : recv[q];
+  }
+  t.par = par;
+  return t;
 }
 
 EpiTarget epi_red(unsigned long long mc) {
@@ -359,8 +385,8 @@ cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* d
   return cudaGetLastError();
 }
 
-cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index) {
-  k_barrier<<<1, 32, 0, st>>>(a->impl->dev, static_cast<uint32_t>(index));
+cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index, int* ctr) {
+  k_barrier<<<1, 32, 0, st>>>(a->impl->dev, static_cast<uint32_t>(index), ctr);
   return cudaGetLastError();
 }
 

@@ -66,8 +66,11 @@ struct OwnerOut {
 };
 // Owner phase: sum the P slots of `slice` elements in `recv` (bf16, or fp32
 // when f32) in rank order 0..P-1 in fp32, round once (bf16), write per `out`.
+// With `par` (kExchange double buffering) the slots come from recv_alt when
+// (*par - 1) is odd: the barrier before the reduce advanced the counter.
 cudaError_t sym_owner_reduce(const void* recv, long long slice, int P, bool f32,
-                             const OwnerOut& out, int num_sms, cudaStream_t st);
+                             const OwnerOut& out, int num_sms, cudaStream_t st,
+                             const int* par = nullptr, const void* recv_alt = nullptr);
 // All-gather pull on the SMs: dst = src[0] | src[1] | ... | src[P-1], each
 // `bytes` long (bytes % 16 == 0; src are LSA peer addresses or local).
 cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* dst, int num_sms,
@@ -80,17 +83,25 @@ cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* d
 // `index` (0 or 1) is its own barrier sequence: every rank must issue the
 // barriers of one index in the same order, and all barriers of one index must
 // be issued on one stream (the epoch state is not safe under concurrency).
-cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0);
+// `ctr` (optional): incremented by one thread after the barrier (kExchange parity).
+cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0, int* ctr = nullptr);
 
 // Fused-reduction plan shared by the multi-GPU path (axonn.cpp) and the
 // single-GPU loopback (loopback.cpp): the epilogue mode of a rows x cols
 // output of a GEMM with contraction length kdim reduced over P ranks with
 // es-byte elements.  kStore means "not fused" (NCCL, or no reduction when
-// P == 1).  2-rank bf16 axes use multimem.red when kdim >= red_min_k.
-int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k);
+// P == 1).  2-rank bf16 axes use multimem.red when kdim >= red_min_k, else
+// (exchange2) the exchange of whole partials, else the scatter + owner phase.
+int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
+               bool exchange2);
 // Epilogue targets: multimem.red into `mc`; scatter of 16-B units to the
 // owners' receive slots peer[0..P) (owner o = flat / slice).
 EpiTarget epi_red(unsigned long long mc);
 EpiTarget epi_scatter(int P, int me, long long slice, const unsigned long long* peer);
+// All-reduce by exchange (2-rank axes): every rank's whole partial into slot
+// `me` of every rank's receive buffer (recv[q]: rank q's buffer of P slots of
+// n elements; recv_alt: the second set, chosen when *par is odd).
+EpiTarget epi_exchange(int P, int me, long long n, const unsigned long long* recv,
+                       const unsigned long long* recv_alt, const int* par);
 
 }  // namespace axonn

@@ -23,8 +23,8 @@ PAPER.md:375-390; data parallelism PAPER.md:313-317):
   fp64 per-rank O, dI, dŴ;
 * every member of a reduction group holds bit-identical bits.
 Grids: every factorisation of G = 2, 3, 4, 6, 8 (P = 2, 3, 4, 6, 8 rank
-axes), normal and transposed, both 2-rank modes (multimem.red forced, and the
-scatter + owner phase), both AG_z paths.
+axes), normal and transposed, all three 2-rank modes (exchange of whole
+partials, multimem.red forced, scatter + owner phase), both AG_z paths.
 """
 import os
 import subprocess
@@ -131,13 +131,19 @@ def rounded_reductions(X, W, dY, cfg, transposed, grad_f32):
     return res, exp
 
 
-def _expected_paths(cfg, transposed, flags):
+def _expected_paths(cfg, transposed, flags, grad_f32=False):
+    """The fused paths the multi-GPU mode selection takes for these shapes
+    (short K): 2-rank axes exchange whole partials (or multimem.red when
+    forced, or scatter + owner phase when exchange is off), wider axes scatter."""
     ax_f, ax_b = (0, 1) if transposed else (1, 0)
     want = set()
-    red2 = bool(flags & 1)
+    red2, no_x = bool(flags & 1), bool(flags & 16)
+
+    def two(name, es2=True):
+        return f"{name}_red" if (red2 and es2) else (f"{name}_scatter" if no_x else f"{name}_exchange")
     for name, P in (("fwd", cfg[ax_f]), ("bwd", cfg[ax_b])):
-        if P == 2 and red2:
-            want.add(f"{name}_red")
+        if P == 2:
+            want.add(two(name))
         elif P > 1:
             want.add(f"{name}_scatter")
     if cfg[2] > 1:
@@ -145,8 +151,10 @@ def _expected_paths(cfg, transposed, flags):
         want.add("gather_pull" if flags & 4 else "gather_copy")
         if cfg[3] > 1:
             want.add("dp_after_rs")
-    elif cfg[3] > 1:
-        want.add("dp_red" if (cfg[3] == 2 and red2) else "dp_scatter")
+    elif cfg[3] == 2:
+        want.add(two("dp", not grad_f32))
+    elif cfg[3] > 2:
+        want.add("dp_scatter")
     return want
 
 
@@ -154,7 +162,7 @@ def check(ax, G, cfg, transposed, kind, flags=0, grad_f32=False, shape=None):
     m, k, n = shape or SHAPES[G]
     (X, W, dY), outs, paths = run_loopback(ax, m, k, n, cfg, transposed, kind, flags, grad_f32)
     tag = f"cfg={cfg} T={transposed} {kind} flags={flags} gradf32={grad_f32}"
-    want = _expected_paths(cfg, transposed, flags)
+    want = _expected_paths(cfg, transposed, flags, grad_f32)
     assert want <= paths, f"{tag}: fused paths {sorted(paths)} lack {sorted(want - paths)}"
     res, exp = rounded_reductions(X, W, dY, cfg, transposed, grad_f32)
     ax_f, ax_b = ("x", "y") if transposed else ("y", "x")
@@ -189,10 +197,12 @@ CASES = [(G, cfg) for G in (2, 3, 4, 6, 8) for cfg in grid.enumerate_configs(G)]
 @pytest.mark.parametrize("transposed", [False, True])
 @pytest.mark.parametrize("G,cfg", CASES, ids=[f"{c[0]}{c[1]}{c[2]}{c[3]}" for _, c in CASES])
 def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
-    # default 2-rank mode for these short K (scatter + owner phase) and the
-    # copy-engine AG_z; then multimem.red forced on 2-rank axes with the SM-pull AG_z
+    # default 2-rank mode for these short K (exchange of whole partials) and
+    # the copy-engine AG_z; multimem.red forced on 2-rank axes with the
+    # SM-pull AG_z; the 2-rank scatter + owner phase (exchange off)
     check(ax, G, cfg, transposed, "int", 0)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE)
 
 
 @pytest.mark.parametrize("transposed", [False, True])
@@ -209,6 +219,7 @@ def test_fp32_gradients_bit_exact(ax, cfg, transposed):
     """AXONN_BF16_GRADF32 (R17): fp32 dW epilogue, fp32 RS_z / DP owner phases."""
     G = int(np.prod(cfg))
     check(ax, G, cfg, transposed, "int", 0, grad_f32=True)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE, grad_f32=True)
     check(ax, G, cfg, transposed, "uniform", 0, grad_f32=True)
 
 
