@@ -116,7 +116,16 @@ typedef struct {
   int dtype;          /* axonn_dtype_t                                            */
   int chunks;         /* forward AR pipelining: M-chunks of the local GEMM whose
                          all-reduce starts as each finishes (0/1 = unchunked).    */
+  int act;            /* axonn_act_t applied to the layer's output (fc1 of a GPT
+                         block: AXONN_ACT_GELU).  0 = none.                       */
 } axonn_fc_desc_t;
+
+/* Activation on a layer's output (reading R18):
+ *   forward  Z = all-reduce(Ô) (Alg. 1 line 4), O_local = GELU(Z),
+ *   backward dZ = dO_local ⊙ GELU'(Z) takes dO's place in lines 11 and 13,
+ * with GELU(x) = x Φ(x) exactly (erf).  Z is rounded to bf16 where Alg. 1
+ * rounds O (R8); the handle keeps Z for the backward.  bf16 layers only. */
+typedef enum { AXONN_ACT_NONE = 0, AXONN_ACT_GELU = 1 } axonn_act_t;
 
 /* Shard geometry of one rank (readings R1, R2, R4, R6):
  *   I_local  = X[row0 : row0+m_l, in_col0 : in_col0+k_l]         ([m_l][k_l])

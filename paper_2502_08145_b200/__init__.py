@@ -29,6 +29,7 @@ AXONN_OK, AXONN_ERR_ARG, AXONN_ERR_CONFIG, AXONN_ERR_SHAPE, AXONN_ERR_STATE = 0,
 AXONN_ERR_INFEASIBLE, AXONN_ERR_CUDA, AXONN_ERR_NCCL, AXONN_ERR_UNSUPPORTED = 5, 6, 7, 8
 AXONN_BF16, AXONN_F32, AXONN_BF16_GRADF32 = 0, 1, 2
 AXONN_OP_NN, AXONN_OP_NT, AXONN_OP_TN = 0, 1, 2
+AXONN_ACT_NONE, AXONN_ACT_GELU = 0, 1
 AXIS = {"x": 0, "y": 1, "z": 2, "d": 3}
 AXONN_LB_RED_ALWAYS, AXONN_LB_RED_NEVER, AXONN_LB_GATHER_PULL, AXONN_LB_EMULATE_MC = 1, 2, 4, 8
 AXONN_LB_NO_EXCHANGE = 16
@@ -49,7 +50,7 @@ class AxonnError(RuntimeError):
 # ---------------------------------------------------------------- structs
 class FcDesc(Structure):
     _fields_ = [("m", c_int64), ("k", c_int64), ("n", c_int64), ("transposed", c_int),
-                ("dtype", c_int), ("chunks", c_int)]
+                ("dtype", c_int), ("chunks", c_int), ("act", c_int)]
 
 
 class GeometryT(Structure):
@@ -193,8 +194,8 @@ def axonn_group_members(rank: int, cfg, axis):
     return tuple(out)
 
 
-def _desc(m, k, n, transposed=False, dtype=AXONN_BF16, chunks=1):
-    return FcDesc(m, k, n, int(bool(transposed)), dtype, chunks)
+def _desc(m, k, n, transposed=False, dtype=AXONN_BF16, chunks=1, act=AXONN_ACT_NONE):
+    return FcDesc(m, k, n, int(bool(transposed)), dtype, chunks, act)
 
 
 def axonn_shard_geometry(m, k, n, cfg, rank, transposed=False, dtype=AXONN_BF16) -> Geometry:
@@ -204,9 +205,10 @@ def axonn_shard_geometry(m, k, n, cfg, rank, transposed=False, dtype=AXONN_BF16)
     return Geometry(*[getattr(g, f) for f in Geometry._fields])
 
 
-def axonn_fc_create(m, k, n, transposed=False, dtype=AXONN_BF16, chunks=1) -> int:
+def axonn_fc_create(m, k, n, transposed=False, dtype=AXONN_BF16, chunks=1,
+                    act=AXONN_ACT_NONE) -> int:
     h = c_void_p()
-    d = _desc(m, k, n, transposed, dtype, chunks)
+    d = _desc(m, k, n, transposed, dtype, chunks, act)
     _check(_lib.axonn_fc_create(byref(d), byref(h)))
     return h.value
 
@@ -266,7 +268,7 @@ def axonn_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, stream=None) -> None:
 
 
 def axonn_loopback_step(m, k, n, cfg, I, W_hat, dO, O, dI, dW, transposed=False,
-                        dtype=AXONN_BF16, flags=0, stream=None) -> set:
+                        dtype=AXONN_BF16, flags=0, stream=None, act=AXONN_ACT_NONE) -> set:
     """Alg. 1 for every rank of grid ``cfg`` on this GPU (include/axonn.h, test
     support).  I, W_hat, dO, O, dI, dW: per-rank lists of tensors (rank order).
     Returns the names of the fused paths that ran (LB_PATHS)."""
@@ -276,7 +278,7 @@ def axonn_loopback_step(m, k, n, cfg, I, W_hat, dO, O, dI, dW, transposed=False,
         if len(lst) != G:
             raise ValueError(f"need {G} per-rank tensors, got {len(lst)}")
         arrs.append((c_void_p * G)(*[_ptr(t).value or 0 for t in lst]))
-    d = _desc(m, k, n, transposed, dtype)
+    d = _desc(m, k, n, transposed, dtype, 1, act)
     paths = c_int()
     _check(_lib.axonn_loopback_step(byref(d), *cfg, *arrs, flags, _stream_ptr(stream),
                                     byref(paths)))

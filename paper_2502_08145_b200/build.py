@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libaxonn.so")
-SOURCES = ["gemm_tc.cu", "gemm_simt.cu", "sym.cu", "perf_model.cpp", "axonn.cpp", "loopback.cpp"]
+SOURCES = ["gemm_tc.cu", "gemm_simt.cu", "sym.cu", "perf_model.cpp", "axonn.cpp", "loopback.cpp", "act.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

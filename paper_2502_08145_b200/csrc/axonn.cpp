@@ -35,6 +35,7 @@
 #include <vector>
 
 #include "../../include/axonn.h"
+#include "act.h"
 #include "gemm.h"
 #include "perf_model.h"
 #include "runtime.h"
@@ -269,6 +270,8 @@ axonn_status_t geometry_of(const axonn_fc_desc_t* d, const int g[4], int rank,
   if (d->m < 0 || d->k < 0 || d->n < 0) return fail(AXONN_ERR_ARG, "negative dimension");
   if (!valid_dtype(d->dtype))
     return fail(AXONN_ERR_ARG, "dtype must be AXONN_BF16, AXONN_F32 or AXONN_BF16_GRADF32");
+  if (d->act != AXONN_ACT_NONE && d->act != AXONN_ACT_GELU)
+    return fail(AXONN_ERR_ARG, "act must be AXONN_ACT_NONE or AXONN_ACT_GELU");
   const int G = g[0] * g[1] * g[2] * g[3];
   if (rank < 0 || rank >= G) return fail(AXONN_ERR_ARG, "rank %d outside grid of %d", rank, G);
   const bool t = d->transposed != 0;
@@ -313,6 +316,8 @@ struct axonn_fc {
   axonn_geometry_t geo;
   int ax_fwd, ax_bwd;         // axis of the forward / backward-dI all-reduce
   void* wbuf = nullptr;       // gathered W_{j,i} when Gz > 1
+  void* zbuf = nullptr;       // act: Z = all-reduce(Ô) kept for the backward (R18)
+  void* dzbuf = nullptr;      // act: dZ = dO ⊙ GELU'(Z)
   void* dwpart = nullptr;     // dW partial when Gz > 1
   const void* I = nullptr;    // cached I_{k,j} (caller-owned)
   const void* W = nullptr;    // W_{j,i} used by the last forward
@@ -500,7 +505,8 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
   return AXONN_OK;  // scatter: the previous use's final barrier already freed the slots
 }
 
-axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
+axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0,
+                          void* act_z = nullptr) {
   if (f.epi.mode == axonn::kExchange) {
     // every rank's whole partial has landed in our slots (the barrier also
     // advances the parity counter); the sum is local, in slot order, so all
@@ -510,6 +516,11 @@ axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0) {
     axonn::OwnerOut o;
     o.n_dst = 1;
     o.dst[0] = reinterpret_cast<unsigned long long>(f.out.ptr);
+    if (act_z) {  // the GeLU rides on the local sum: Z to act_z, GELU(Z) to the output
+      o.dst[0] = reinterpret_cast<unsigned long long>(act_z);
+      o.act = 1;
+      o.act_dst = reinterpret_cast<unsigned long long>(f.out.ptr);
+    }
     CUDA_TRY(axonn::sym_owner_reduce(f.recv.ptr, static_cast<long long>(f.elems), f.epi.P,
                                      f.es == 4, o, S.num_sms, st, f.par, f.recv2.ptr));
     g_launches.fetch_add(1);
@@ -576,6 +587,13 @@ axonn_status_t issue_allgather(axonn_fc* h, const void* W_hat, cudaStream_t st) 
   return AXONN_OK;
 }
 
+// O_local holds Z = all-reduce(Ô): keep Z for the backward, O_local := GELU(Z)
+axonn_status_t apply_act(axonn_fc* h, void* O_local, cudaStream_t st) {
+  CUDA_TRY(axonn::gelu_forward_inplace(O_local, h->zbuf, h->geo.m_l * h->geo.n_l, S.num_sms, st));
+  g_launches.fetch_add(1);
+  return AXONN_OK;
+}
+
 }  // namespace
 
 namespace axonn {
@@ -592,7 +610,7 @@ int rt_num_sms() { return S.num_sms; }
 extern "C" {
 
 const char* axonn_last_error(void) { return g_err.c_str(); }
-int axonn_version(void) { return 100; }
+int axonn_version(void) { return 200; }
 
 axonn_status_t axonn_unique_id(unsigned char id[128]) {
   if (!id) return fail(AXONN_ERR_ARG, "NULL id");
@@ -771,6 +789,13 @@ axonn_status_t axonn_fc_create(const axonn_fc_desc_t* desc, axonn_fc_t* out) {
     return s;
   };
   S.handles.insert(h);
+  if (desc->act != AXONN_ACT_NONE) {
+    if (desc->dtype == AXONN_F32)
+      return cleanup(fail(AXONN_ERR_UNSUPPORTED, "an activation needs bf16 activations"));
+    const size_t zb = static_cast<size_t>(geo.m_l) * geo.n_l * 2;
+    if (zb && (cudaMalloc(&h->zbuf, zb) != cudaSuccess || cudaMalloc(&h->dzbuf, zb) != cudaSuccess))
+      return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", 2 * zb));
+  }
   if (S.g[AX_Z] > 1 && wbytes) {
     if (cudaMalloc(&h->wbuf, wbytes) != cudaSuccess || cudaMalloc(&h->dwpart, gbytes) != cudaSuccess)
       return cleanup(fail(AXONN_ERR_CUDA, "cudaMalloc of %zu bytes failed", wbytes + gbytes));
@@ -947,10 +972,12 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
     STATUS_TRY(fused_pre(h->fo, st));
     STATUS_TRY(run_gemm(AXONN_OP_NN, act_dtype(h->d.dtype), g.m_l, g.n_l, g.k_l, I_local, g.k_l, W, g.n_l,
                         h->fo.out.ptr, g.n_l, st, &h->fo.epi));
-    STATUS_TRY(fused_post(h->fo, st));
+    const bool act_fused = h->zbuf && h->fo.epi.mode == axonn::kExchange;
+    STATUS_TRY(fused_post(h->fo, st, 0, act_fused ? h->zbuf : nullptr));
     count_comm(2, P, static_cast<size_t>(g.m_l * g.n_l), h->d.dtype);
     if (O_local != h->fo.out.ptr)
       CUDA_TRY(cudaMemcpyAsync(O_local, h->fo.out.ptr, bytes, cudaMemcpyDeviceToDevice, st));
+    if (h->zbuf && !act_fused) STATUS_TRY(apply_act(h, O_local, st));
     h->I = I_local;
     h->W = W;
     h->have_fwd = true;
@@ -983,6 +1010,7 @@ axonn_status_t axonn_fc_forward(axonn_fc_t h, const void* I_local, const void* W
     CUDA_TRY(cudaEventRecord(h->ev_ar, cs));
     CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ar, 0));
   }
+  if (h->zbuf) STATUS_TRY(apply_act(h, O_local, st));
   // line 5: cache I_{k,j} and W_{j,i}
   h->I = I_local;
   h->W = W;
@@ -1001,6 +1029,12 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     return fail(AXONN_ERR_ARG, "NULL tensor");
   STATUS_TRY(check_async_nccl());
   cudaStream_t st = as_stream(stream);
+  if (h->zbuf && g.m_l != 0 && g.n_l != 0) {
+    // dZ = dO ⊙ GELU'(Z) replaces dO in lines 11 and 13 (R18)
+    CUDA_TRY(axonn::gelu_backward(dO_local, h->zbuf, h->dzbuf, g.m_l * g.n_l, S.num_sms, st));
+    g_launches.fetch_add(1);
+    dO_local = h->dzbuf;
+  }
   const int dt = h->d.dtype;
   const ncclDataType_t nt = nccl_type(dt);
   const int gdt = grad_dtype(dt);             // dWpart / dŴ and their reductions
@@ -1179,6 +1213,8 @@ axonn_status_t axonn_fc_destroy(axonn_fc_t h) {
     if (e) cudaEventDestroy(e);
   if (h->wbuf) cudaFree(h->wbuf);
   if (h->dwpart) cudaFree(h->dwpart);
+  if (h->zbuf) cudaFree(h->zbuf);
+  if (h->dzbuf) cudaFree(h->dzbuf);
   for (axonn_fc::Fused* f : {&h->fo, &h->fi, &h->fw, &h->fz, &h->fd}) fused_reset(f);
   axonn::sym_free(&S.sym[AX_Z], &h->wstage);
   delete h;

@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "../../include/axonn.h"
+#include "act.h"
 #include "gemm.h"
 #include "runtime.h"
 #include "sym.h"
@@ -405,13 +406,19 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
         return rt_fail(AXONN_ERR_CUDA, "loopback: memset failed");
     return AXONN_OK;
   };
-  // every rank's owner phase (scatter mode)
-  auto owner_phase = [&](const LbOp& op) -> axonn_status_t {
+  // every rank's owner phase (scatter mode) or local sum (exchange mode);
+  // act_z: the forward GeLU rides on the exchange's local sum (Z -> act_z[r])
+  auto owner_phase = [&](const LbOp& op, const std::vector<void*>* act_z = nullptr) -> axonn_status_t {
     if (op.mode == kExchange) {  // every rank sums its own P slots locally
       for (int r = 0; r < G; ++r) {
         OwnerOut o;
         o.n_dst = 1;
         o.dst[0] = reinterpret_cast<unsigned long long>(op.out[r]);
+        if (act_z) {
+          o.dst[0] = reinterpret_cast<unsigned long long>((*act_z)[r]);
+          o.act = 1;
+          o.act_dst = reinterpret_cast<unsigned long long>(op.out[r]);
+        }
         if (sym_owner_reduce(op.recv[r], op.elems, op.P, op.es == 4, o, rt_num_sms(), st) !=
             cudaSuccess)
           return rt_fail(AXONN_ERR_CUDA, "loopback: exchange sum launch failed");
@@ -465,6 +472,17 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     for (int r = 0; r < G; ++r) Wfull[r] = What[r];
   }
 
+  // activation (fc1's GeLU, reading R18): Z kept per rank, dZ formed per rank
+  const bool act = d->act == AXONN_ACT_GELU;
+  std::vector<void*> zbuf(G, nullptr), dzbuf(G, nullptr);
+  if (act) {
+    for (int r = 0; r < G; ++r) {
+      zbuf[r] = pool.get(m_l * n_l * 2);
+      dzbuf[r] = pool.get(m_l * n_l * 2);
+      if (!zbuf[r] || !dzbuf[r]) return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
+    }
+  }
+
   // ------------------------------------------------ lines 3-4: Ô, AR (Eq. 3)
   if ((s = zero_regions(fo)) != AXONN_OK) return s;
   for (int r = 0; r < G; ++r) {
@@ -474,19 +492,37 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
                      fo.mode == kStore ? nullptr : &t)) != AXONN_OK)
       return s;
   }
-  if ((s = owner_phase(fo)) != AXONN_OK) return s;
+  const bool act_fused = act && fo.mode == kExchange;
+  if ((s = owner_phase(fo, act_fused ? &zbuf : nullptr)) != AXONN_OK) return s;
   if (fo.mode != kStore) {
     p |= fo.mode == kMcRed ? AXONN_LB_PATH_FWD_RED
          : fo.mode == kExchange ? AXONN_LB_PATH_FWD_EXCHANGE : AXONN_LB_PATH_FWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fo, r, O[r])) != AXONN_OK) return s;
   }
+  if (act && !act_fused) {  // O holds Z: keep it, O := GELU(Z)
+    for (int r = 0; r < G; ++r) {
+      if (gelu_forward_inplace(O[r], zbuf[r], m_l * n_l, rt_num_sms(), st) != cudaSuccess)
+        return rt_fail(AXONN_ERR_CUDA, "loopback: GeLU launch failed");
+      rt_count_launch();
+    }
+  }
+  // backward of the activation: dZ = dO ⊙ GELU'(Z) replaces dO in lines 11, 13
+  std::vector<const void*> dOa(dO, dO + G);
+  if (act) {
+    for (int r = 0; r < G; ++r) {
+      if (gelu_backward(dO[r], zbuf[r], dzbuf[r], m_l * n_l, rt_num_sms(), st) != cudaSuccess)
+        return rt_fail(AXONN_ERR_CUDA, "loopback: dGeLU launch failed");
+      rt_count_launch();
+      dOa[r] = dzbuf[r];
+    }
+  }
 
   // ------------------------------------------------ lines 11-12: dÎ, AR (Eq. 4)
   if ((s = zero_regions(fi)) != AXONN_OK) return s;
   for (int r = 0; r < G; ++r) {
     const EpiTarget t = target(fi, r);
-    if ((s = rt_gemm(AXONN_OP_NT, AXONN_BF16, m_l, k_l, n_l, dO[r], n_l, Wfull[r], n_l,
+    if ((s = rt_gemm(AXONN_OP_NT, AXONN_BF16, m_l, k_l, n_l, dOa[r], n_l, Wfull[r], n_l,
                      fi.mode == kStore ? dI[r] : nullptr, k_l, st,
                      fi.mode == kStore ? nullptr : &t)) != AXONN_OK)
       return s;
@@ -514,7 +550,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       t = target(fw, r);
       tp = &t;
     }
-    if ((s = rt_gemm(AXONN_OP_TN, d->dtype, k_l, n_l, m_l, I[r], k_l, dO[r], n_l,
+    if ((s = rt_gemm(AXONN_OP_TN, d->dtype, k_l, n_l, m_l, I[r], k_l, dOa[r], n_l,
                      tp ? nullptr : dW[r], n_l, st, tp)) != AXONN_OK)
       return s;
   }

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <string>
 
+#include "act.h"
 #include "sym.h"
 
 namespace axonn {
@@ -118,6 +119,16 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv0, const uint4* __r
     } else {
       for (int d = 0; d < out.n_dst; ++d)
         reinterpret_cast<uint4*>(out.dst[d])[i] = r;
+      if (!F32 && out.act) {  // GELU of the rounded sum (act.cu, R18)
+        uint32_t a[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(gelu_f(__uint_as_float(o[q] << 16)),
+                                                    gelu_f(__uint_as_float(o[q] & 0xFFFF0000u)));
+          a[q] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        reinterpret_cast<uint4*>(out.act_dst)[i] = make_uint4(a[0], a[1], a[2], a[3]);
+      }
     }
   }
   asm volatile("fence.acq_rel.sys;" ::: "memory");

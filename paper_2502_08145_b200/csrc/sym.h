@@ -63,6 +63,10 @@ struct OwnerOut {
   unsigned long long dst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int me2 = 0;
   long long slice2 = 0;
+  // kOwnPlain, bf16 only: also write GELU(sum) to act_dst + 16u (the sum
+  // itself still goes to dst[], e.g. Z saved for the backward; reading R18)
+  int act = 0;
+  unsigned long long act_dst = 0;
 };
 // Owner phase: sum the P slots of `slice` elements in `recv` (bf16, or fp32
 // when f32) in rank order 0..P-1 in fp32, round once (bf16), write per `out`.

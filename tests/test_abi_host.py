@@ -198,7 +198,7 @@ def test_header_is_plain_c_and_links(tmp_path):
 #include "axonn.h"
 int main(void) {
   int c[4];
-  axonn_fc_desc_t d = {4096, 1024, 512, 1, AXONN_BF16, 1};
+  axonn_fc_desc_t d = {4096, 1024, 512, 1, AXONN_BF16, 1, AXONN_ACT_NONE};
   axonn_geometry_t g;
   axonn_layer_t L = {16384, 4096, 4096, 0};
   axonn_bw_entry_t tb = {1, 2, 1e11};

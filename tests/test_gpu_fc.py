@@ -182,3 +182,91 @@ def test_ragged_token_counts(ax, m):
     (X, W, dY), outs = _layer(ax, m, 136, 264, False, "int", torch.bfloat16)
     for got, ref in zip(outs, fc.fc_layer(X, W, dY)):
         assert np.array_equal(bf16_bits_of(got), synthdata.bf16_bits(synthdata.bf16_round(ref)))
+
+
+@pytest.mark.parametrize("m,k,n", [(256, 512, 1024), (384, 200, 136)])
+def test_gelu_layer_g1(ax, m, k, n):
+    """fc1's GeLU through the ABI at G = 1 (reading R18): O = GELU(X W) and the
+    backward on dZ = dY ⊙ GELU'(X W), against oracle.act; the activation pass
+    itself against GELU of the GPU's own Z within one bf16 ulp."""
+    torch = require_cuda()
+    from oracle import act
+    X, W, dY = synthdata.layer_tensors(m, k, n, 4, kind="uniform")
+    h = ax.axonn_fc_create(m, k, n, False, ax.AXONN_BF16, 1, ax.AXONN_ACT_GELU)
+    I, What, dO = to_dev(X, torch.bfloat16), to_dev(W.reshape(1, -1), torch.bfloat16).reshape(-1), \
+        to_dev(dY, torch.bfloat16)
+    O = empty_dev(m, n, torch.bfloat16)
+    dI = empty_dev(m, k, torch.bfloat16)
+    dW = empty_dev(1, k * n, torch.bfloat16).reshape(-1)
+    ax.axonn_fc_forward(h, I, What, O)
+    ax.axonn_fc_backward(h, dO, dI, dW)
+    ax.axonn_grads_sync()
+    torch.cuda.synchronize()
+    ax.axonn_fc_destroy(h)
+    Z = fc.fc_forward(X, W)
+    dZ = dY * act.gelu_grad(Z)
+    for name, got, ref in (("O", O, act.gelu(Z)), ("dI", dI, fc.fc_backward_input(dZ, W)),
+                           ("dW", dW.reshape(k, n), fc.fc_backward_weight(X, dZ))):
+        e = normwise_err(to_host_f64(got), ref)
+        assert e <= 2e-2, (name, e)
+
+
+def test_gelu_activation_pass_g1(ax):
+    """The activation pass itself: on integer inputs Z = X W is exact and
+    bf16(Z) is the same on both sides, so O must be bf16(GELU(bf16(Z))) up to
+    one bf16 ulp plus the fp32 cancellation of 1 + erf(x/√2) for x < 0
+    (absolute |x|·2^-22)."""
+    torch = require_cuda()
+    from oracle import act
+    m, k, n = 256, 64, 512
+    X, W, dY = synthdata.layer_tensors(m, k, n, 5, kind="int")
+    X = X / 4.0            # Z in [-64, 64]: the whole GeLU range is exercised
+    h = ax.axonn_fc_create(m, k, n, False, ax.AXONN_BF16, 1, ax.AXONN_ACT_GELU)
+    I, What, dO = to_dev(X, torch.bfloat16), to_dev(W.reshape(1, -1), torch.bfloat16).reshape(-1), \
+        to_dev(dY, torch.bfloat16)
+    O = empty_dev(m, n, torch.bfloat16)
+    dI = empty_dev(m, k, torch.bfloat16)
+    dW = empty_dev(1, k * n, torch.bfloat16).reshape(-1)
+    ax.axonn_fc_forward(h, I, What, O)
+    ax.axonn_fc_backward(h, dO, dI, dW)
+    torch.cuda.synchronize()
+    ax.axonn_fc_destroy(h)
+    Zb = synthdata.bf16_round(fc.fc_forward(X, W)).astype(np.float64)
+    want = act.gelu(Zb)
+    got = to_host_f64(O)
+    tol = np.abs(want) * 2.0 ** -7 + np.abs(Zb) * 2.0 ** -22
+    assert np.all(np.abs(got - want) <= tol), np.max(np.abs(got - want) - tol)
+
+
+def test_gelu_mlp_chain_g1(ax):
+    """fc1 (GeLU) -> fc2 chained on device at G = 1 vs oracle.act.mlp."""
+    torch = require_cuda()
+    from oracle import act
+    m, h = 256, 128
+    X = synthdata.tensor((m, h), 31)
+    W1 = synthdata.bf16_round(synthdata.tensor((h, 4 * h), 32) * 0.1)
+    W2 = synthdata.bf16_round(synthdata.tensor((4 * h, h), 33) * 0.05)
+    dY = synthdata.tensor((m, h), 34)
+    h1 = ax.axonn_fc_create(m, h, 4 * h, False, ax.AXONN_BF16, 1, ax.AXONN_ACT_GELU)
+    h2 = ax.axonn_fc_create(m, 4 * h, h, True, ax.AXONN_BF16)
+    dev = lambda a: to_dev(a, torch.bfloat16)  # noqa: E731
+    Xd, W1d, W2d, dYd = dev(X), dev(W1.reshape(1, -1)).reshape(-1), dev(W2.reshape(1, -1)).reshape(-1), dev(dY)
+    A = empty_dev(m, 4 * h, torch.bfloat16)
+    O = empty_dev(m, h, torch.bfloat16)
+    dA = empty_dev(m, 4 * h, torch.bfloat16)
+    dX = empty_dev(m, h, torch.bfloat16)
+    dW1 = empty_dev(1, h * 4 * h, torch.bfloat16).reshape(-1)
+    dW2 = empty_dev(1, h * 4 * h, torch.bfloat16).reshape(-1)
+    ax.axonn_fc_forward(h1, Xd, W1d, A)
+    ax.axonn_fc_forward(h2, A, W2d, O)
+    ax.axonn_fc_backward(h2, dYd, dA, dW2)
+    ax.axonn_fc_backward(h1, dA, dX, dW1)
+    ax.axonn_grads_sync()
+    torch.cuda.synchronize()
+    for hh in (h1, h2):
+        ax.axonn_fc_destroy(hh)
+    r = act.mlp(X, W1, W2, dY)
+    for name, got, ref in (("O", O, r["O"]), ("dX", dX, r["dX"]), ("dW1", dW1.reshape(h, 4 * h), r["dW1"]),
+                           ("dW2", dW2.reshape(4 * h, h), r["dW2"])):
+        e = normwise_err(to_host_f64(got), ref)
+        assert e <= 2e-2, (name, e)

@@ -333,3 +333,60 @@ def test_full_size_tensor_parallel(ax, name, h, m, cfg, which):
             assert max(e_o, e_i, e_w) <= 2e-2, (name, li, r, e_o, e_i, e_w)
         del I, Wh, dO, O, dI, dW, X, W, dY
         torch.cuda.empty_cache()
+
+
+def check_act(ax, G, cfg, transposed, flags=0):
+    """fc1's GeLU on the layer output (reading R18): O = GELU(Z), Z = the
+    all-reduce of line 4; the backward runs lines 11-14 on dZ = dO ⊙ GELU'(Z).
+    The oracle: alg1.simulate gives each rank's Z; the backward is simulated
+    with the global dZ = dY ⊙ GELU'(X W) (oracle.act)."""
+    from oracle import act
+    m, k, n = SHAPES[G]
+    (X, W, dY), outs, paths = run_loopback_act(ax, m, k, n, cfg, transposed, flags)
+    Zg = fc.fc_forward(X, W)
+    dZ = dY * act.gelu_grad(Zg)
+    resZ = alg1.simulate(X, W, dY, cfg, transposed)
+    resB = alg1.simulate(X, W, dZ, cfg, transposed)
+    tag = f"act cfg={cfg} T={transposed} flags={flags}"
+    for r in range(G):
+        O, dI, dW = outs[r]
+        for name, got, ref in (("O", O, act.gelu(resZ.O[r])), ("dI", dI, resB.dI[r]),
+                               ("dW", dW, resB.dW_hat[r])):
+            e = normwise_err(got, ref.reshape(got.shape))
+            assert e <= 2e-2, f"{tag}: rank {r} {name} normwise {e:.3e}"
+    return paths
+
+
+def run_loopback_act(ax, m, k, n, cfg, transposed, flags):
+    torch = require_cuda()
+    X, W, dY = synthdata.layer_tensors(m, k, n, 9, kind="uniform")
+    G = int(np.prod(cfg))
+    I, Wh, dO, O, dI, dW = [], [], [], [], [], []
+    for r in range(G):
+        g = ax.axonn_shard_geometry(m, k, n, cfg, r, transposed)
+        I.append(_dev(ax, X[g.row0:g.row0 + g.m_l, g.in_col0:g.in_col0 + g.k_l], torch.bfloat16))
+        Wl = np.ascontiguousarray(W[g.in_col0:g.in_col0 + g.k_l, g.out_col0:g.out_col0 + g.n_l])
+        Wh.append(_dev(ax, Wl.reshape(-1)[g.what_off:g.what_off + g.what_len], torch.bfloat16))
+        dO.append(_dev(ax, dY[g.row0:g.row0 + g.m_l, g.out_col0:g.out_col0 + g.n_l], torch.bfloat16))
+        O.append(torch.full((g.m_l, g.n_l), float("nan"), dtype=torch.bfloat16, device="cuda"))
+        dI.append(torch.full((g.m_l, g.k_l), float("nan"), dtype=torch.bfloat16, device="cuda"))
+        dW.append(torch.full((g.what_len,), float("nan"), dtype=torch.bfloat16, device="cuda"))
+    paths = ax.axonn_loopback_step(m, k, n, cfg, I, Wh, dO, O, dI, dW, transposed, ax.AXONN_BF16,
+                                   flags, act=ax.AXONN_ACT_GELU)
+    outs = {r: (_host(O[r]), _host(dI[r]), _host(dW[r])) for r in range(G)}
+    return (X, W, dY), outs, paths
+
+
+@pytest.mark.parametrize("cfg", [(1, 1, 1, 1), (1, 2, 1, 1), (2, 1, 1, 1), (1, 4, 1, 1),
+                                 (2, 2, 1, 1), (1, 2, 2, 1), (2, 1, 2, 2), (1, 1, 2, 2)])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_gelu_layer(ax, cfg, transposed):
+    """GeLU fused into the exchange's local sum (2-rank forward axes), or the
+    elementwise pass after the other forward modes; dGeLU before line 11."""
+    G = int(np.prod(cfg))
+    paths = check_act(ax, G, cfg, transposed, 0)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_RED_ALWAYS)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE)
+    ax_f = 0 if transposed else 1
+    if cfg[ax_f] == 2:
+        assert "fwd_exchange" in paths
