@@ -269,8 +269,11 @@ enum {
   AXONN_LB_RED_NEVER = 2,    /* never multimem.red: scatter + owner phase        */
   AXONN_LB_GATHER_PULL = 4,  /* AG_z by the SM pull kernel (else copy engines)   */
   AXONN_LB_EMULATE_MC = 8,   /* no multicast object: red.global.add / plain st   */
-  AXONN_LB_NO_EXCHANGE = 16  /* 2-rank axes below the red threshold: scatter +
+  AXONN_LB_NO_EXCHANGE = 16, /* 2-rank axes below the red threshold: scatter +
                                 owner phase instead of the exchange of partials */
+  AXONN_LB_PAIRSUM = 32,     /* 2-rank bf16 axes: the sum finished in the epilogue */
+  AXONN_LB_REVERSE = 64      /* run each phase's ranks in reverse order (the
+                                pair-sum's second arriver is then rank 0)     */
 };
 enum {
   AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,
@@ -281,7 +284,9 @@ enum {
   AXONN_LB_PATH_GATHER_COPY = 256, AXONN_LB_PATH_GATHER_PULL = 512,
   AXONN_LB_PATH_MULTICAST = 1024,  /* a real one-device multicast object was used */
   AXONN_LB_PATH_FWD_EXCHANGE = 2048, AXONN_LB_PATH_BWD_EXCHANGE = 4096,
-  AXONN_LB_PATH_DP_EXCHANGE = 8192
+  AXONN_LB_PATH_DP_EXCHANGE = 8192,
+  AXONN_LB_PATH_FWD_PAIRSUM = 16384, AXONN_LB_PATH_BWD_PAIRSUM = 32768,
+  AXONN_LB_PATH_DP_PAIRSUM = 65536
 };
 axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
                                    const void* const* I_local, const void* const* W_hat,

@@ -336,6 +336,9 @@ struct axonn_fc {
     axonn::SymBuf recv;   // P-rank scatter mode: P slots of elems / P; exchange: P slots of elems
     axonn::SymBuf recv2;  // exchange mode: the second receive buffer (device-side parity)
     int* par = nullptr;   // exchange mode: parity counter, advanced by the post barrier
+    axonn::SymBuf ctrl;   // pair-sum mode: arbitration tickets + done / call counters
+    long long chunks = 0; // pair-sum mode: 32 x 64 output chunks
+    int64_t cols = 0;     // row length of the reduced output
     axonn::EpiTarget epi;
   };
   Fused fo;   // O   over the forward axis      (Alg. 1 line 4 fused into line 3)
@@ -392,9 +395,19 @@ void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_
   if (!S.sym[axis].impl) return;
   const int mode = axonn::fused_mode(S.g[axis], es, rows, cols, kdim,
                                      env_int("AXONN_RED_MIN_K", 8192),
-                                     env_int("AXONN_EXCHANGE", 1) != 0);
+                                     env_int("AXONN_EXCHANGE", 1) != 0,
+                                     env_int("AXONN_PAIRSUM", 0) != 0);
   if (mode == axonn::kStore) return;
   f->elems = static_cast<size_t>(rows * cols);
+  f->cols = cols;
+  if (mode == axonn::kPairSum) {
+    f->chunks = ((rows + 31) / 32) * ((cols + 63) / 64);
+    f->epi.mode = mode;
+    reqs->push_back({axis, f->elems * es, &f->out});
+    reqs->push_back({axis, f->elems * es, &f->recv});
+    reqs->push_back({axis, axonn::pair_ctrl_bytes(f->chunks), &f->ctrl});
+    return;
+  }
   f->epi.mode = mode;  // targets are bound after registration (fused_bind)
   reqs->push_back({axis, f->elems * es, &f->out});
   if (mode == axonn::kScatter) reqs->push_back({axis, f->elems * es, &f->recv});
@@ -414,6 +427,36 @@ bool fused_bind(axonn_fc::Fused* f, std::string* why) {
     return true;
   }
   const int P = S.g[f->axis], me = S.c[f->axis];
+  if (f->epi.mode == axonn::kPairSum) {
+    char* precv = static_cast<char*>(axonn::sym_peer_ptr(&f->recv, 1 - me));
+    char* pout = static_cast<char*>(axonn::sym_peer_ptr(&f->out, 1 - me));
+    char* pctrl = static_cast<char*>(axonn::sym_peer_ptr(&f->ctrl, 1 - me));
+    char* arb = static_cast<char*>(axonn::sym_peer_ptr(&f->ctrl, 0));
+    if (!precv || !pout || !pctrl || !arb) {
+      *why = "peer address of a pair-sum window unavailable";
+      return false;
+    }
+    if (cudaMemset(f->ctrl.ptr, 0, axonn::pair_ctrl_bytes(f->chunks)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+      *why = "zeroing the pair-sum control block failed";
+      return false;
+    }
+    axonn::EpiTarget t;
+    t.mode = axonn::kPairSum;
+    t.P = 2;
+    t.me = me;
+    t.slice = (f->cols + 63) / 64;
+    t.mc = reinterpret_cast<unsigned long long>(arb);
+    const size_t done = axonn::pair_done_off(f->chunks);
+    t.peer[0] = reinterpret_cast<unsigned long long>(f->recv.ptr);
+    t.peer[1] = reinterpret_cast<unsigned long long>(precv);
+    t.peer[2] = reinterpret_cast<unsigned long long>(f->out.ptr);
+    t.peer[3] = reinterpret_cast<unsigned long long>(pout);
+    t.peer[4] = reinterpret_cast<unsigned long long>(static_cast<char*>(f->ctrl.ptr) + done);
+    t.peer[5] = reinterpret_cast<unsigned long long>(pctrl + done);
+    f->epi = t;
+    return true;
+  }
   unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < P; ++q) {
     peer[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv, q));
@@ -475,6 +518,7 @@ void fused_reset(axonn_fc::Fused* f) {
   axonn::sym_free(&S.sym[f->axis], &f->out);
   axonn::sym_free(&S.sym[f->axis], &f->recv);
   axonn::sym_free(&S.sym[f->axis], &f->recv2);
+  axonn::sym_free(&S.sym[f->axis], &f->ctrl);
   if (f->par) cudaFree(f->par);
   f->par = nullptr;
   f->epi = axonn::EpiTarget();
@@ -507,6 +551,16 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
 
 axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0,
                           void* act_z = nullptr) {
+  if (f.epi.mode == axonn::kPairSum) {
+    // the epilogues of both ranks finished the sums; wait for the peer's
+    // share of the chunks (no barrier, no pass over the output)
+    char* c = static_cast<char*>(f.ctrl.ptr);
+    CUDA_TRY(axonn::sym_pair_wait(c + axonn::pair_done_off(f.chunks),
+                                  c + axonn::pair_calls_off(f.chunks),
+                                  static_cast<uint32_t>(f.chunks), st));
+    g_launches.fetch_add(1);
+    return AXONN_OK;
+  }
   if (f.epi.mode == axonn::kExchange) {
     // every rank's whole partial has landed in our slots (the barrier also
     // advances the parity counter); the sum is local, in slot order, so all

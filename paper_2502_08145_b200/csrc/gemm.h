@@ -21,6 +21,15 @@ namespace axonn {
 //              the post phase is a local sum of the P slots (2-rank axes).
 //              With `par` set, the kernel reads *par and targets peer_alt
 //              instead when it is odd (device-side double buffering).
+//   kPairSum   2-rank all-reduce finished inside the epilogue: each warp's
+//              32x64 chunk goes to the peer's receive buffer (peer[1]), then
+//              one lane takes a ticket on the chunk's arbitration counter
+//              (atomic at mc + 4*chunk, shared by both ranks); the rank that
+//              arrives second adds the peer's partial (its own receive
+//              buffer, peer[0]) and writes the rounded sum to both ranks'
+//              outputs (peer[2] own, peer[3] peer's), then counts the chunk
+//              done on both ranks (peer[4] own counter, peer[5] peer's).
+//              slice = chunks per row of 64 columns.  bf16, ldc == N.
 //   kRedLocal  red.global.add of each 16-B bf16 vector at mc + offset: the
 //              single-GPU loopback's stand-in for kMcRed when the device
 //              has no multicast support (axonn_loopback_step).
@@ -33,7 +42,7 @@ struct EpiTarget {
   unsigned long long peer_alt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int* par = nullptr;
 };
-enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4 };
+enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4, kPairSum = 5 };
 
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 

@@ -597,6 +597,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           __syncwarp();
           const int u = lane & 7;
           const int gcol = tc.n0 + c * CCOLS + u * UCOLS;
+          if (epi.mode == kPairSum) {
+            // 2-rank all-reduce completed in the epilogue (see gemm.h): no
+            // pass over the output after the GEMM, no barrier
+            const int ccol0 = tc.n0 + c * CCOLS;
+            if (row0 < M && ccol0 < N) {
+#pragma unroll 2
+              for (int it = 0; it < 8; ++it) {  // our partial -> the peer's receive buffer
+                const int r = it * 4 + (lane >> 3);
+                const int grow = row0 + r;
+                if (grow < M && gcol < N) {
+                  uint4 w;
+                  const uint32_t a = stage_u32 + r * 128 + ((u ^ (r & 7)) << 4);
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(a) : "memory");
+                  *reinterpret_cast<uint4*>(epi.peer[1] + (static_cast<uint64_t>(grow) * N + gcol) * 2) = w;
+                }
+              }
+              ptx::fence_sys();
+              __syncwarp();
+              uint32_t ticket = 0;
+              const uint64_t chunk = static_cast<uint64_t>(row0 / 32) * epi.slice + ccol0 / CCOLS;
+              if (lane == 0) ticket = ptx::atom_add_acqrel_sys(epi.mc + 4 * chunk, 1u);
+              ticket = __shfl_sync(0xffffffffu, ticket, 0);
+              if (ticket & 1u) {  // second to arrive: the peer's partial has landed here
+                ptx::fence_sys();
+#pragma unroll 2
+                for (int it = 0; it < 8; ++it) {
+                  const int r = it * 4 + (lane >> 3);
+                  const int grow = row0 + r;
+                  if (grow < M && gcol < N) {
+                    uint4 w;
+                    const uint32_t a = stage_u32 + r * 128 + ((u ^ (r & 7)) << 4);
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(a) : "memory");
+                    const uint64_t off = (static_cast<uint64_t>(grow) * N + gcol) * 2;
+                    uint4 p;  // written by the peer over NVLink: bypass L1
+                    asm volatile("ld.volatile.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(p.x), "=r"(p.y), "=r"(p.z), "=r"(p.w)
+                                 : "l"(epi.peer[0] + off) : "memory");
+                    const uint4 f = ptx::add_bf16x8(w, p);
+                    *reinterpret_cast<uint4*>(epi.peer[2] + off) = f;
+                    *reinterpret_cast<uint4*>(epi.peer[3] + off) = f;
+                  }
+                }
+                ptx::fence_sys();
+                __syncwarp();
+                if (lane == 0) {
+                  ptx::red_add_release_sys(epi.peer[4], 1u);
+                  ptx::red_add_release_sys(epi.peer[5], 1u);
+                }
+              }
+            }
+            __syncwarp();
+            continue;
+          }
 #pragma unroll 2
           for (int it = 0; it < 8; ++it) {
             const int r = it * 4 + (lane >> 3);
@@ -861,6 +916,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode == kScatter && (ldc != N || epi.slice % unit || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   if (epi.mode == kExchange && (ldc != N || epi.slice != M * N || epi.P < 1 || epi.P > 8))
+    return GemmStatus::kBadAlignment;
+  if (epi.mode == kPairSum && (out_f32 || ldc != N || epi.slice != (N + 63) / 64))
     return GemmStatus::kBadAlignment;
   // MT=2's single accumulator serialises the epilogue with the next tile; on
   // short K loops that costs more than its lower L2/DRAM traffic saves

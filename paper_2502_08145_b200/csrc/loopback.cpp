@@ -226,6 +226,9 @@ struct LbOp {
   int axis = 0, P = 1, es = 2, mode = kStore;
   int64_t elems = 0;
   std::vector<char*> recv, out;  // per rank (scatter mode)
+  std::vector<char*> ctrl;       // per rank (pair-sum mode): tickets, done, calls
+  int64_t cols = 0;
+  long long chunks = 0;
   std::map<int, size_t> region;  // group leader rank -> arena offset (red, or P >= 3 owner output)
 };
 
@@ -267,6 +270,10 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   bool exchange2 = true;
   if (const char* v = std::getenv("AXONN_EXCHANGE")) exchange2 = std::atoi(v) != 0;
   if (flags & AXONN_LB_NO_EXCHANGE) exchange2 = false;
+  bool pairsum2 = false;
+  if (const char* v = std::getenv("AXONN_PAIRSUM")) pairsum2 = std::atoi(v) != 0;
+  if (flags & AXONN_LB_PAIRSUM) pairsum2 = true;
+  const bool reverse = (flags & AXONN_LB_REVERSE) != 0;
   auto members = [&](int r, int axis) {
     std::vector<int> m(g[axis]);
     axonn_group_members(r, g[0], g[1], g[2], g[3], axis, m.data());
@@ -284,7 +291,9 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     op->es = es;
     op->elems = rows * cols;
     if (op->P == 1) return AXONN_OK;
-    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2);
+    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2, pairsum2);
+    op->cols = cols;
+    op->chunks = ((rows + 31) / 32) * ((cols + 63) / 64);
     if (op->mode == kStore) {
       char buf[200];
       std::snprintf(buf, sizeof buf,
@@ -335,6 +344,20 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
         }
       }
     }
+    if (op->mode == kPairSum) {
+      op->recv.resize(G);
+      op->out.resize(G);
+      op->ctrl.resize(G);
+      for (int r = 0; r < G; ++r) {
+        op->recv[r] = static_cast<char*>(pool.get(op->elems * op->es));
+        op->out[r] = static_cast<char*>(pool.get(op->elems * op->es));
+        op->ctrl[r] = static_cast<char*>(pool.get(pair_ctrl_bytes(op->chunks)));
+        if (!op->recv[r] || !op->out[r] || !op->ctrl[r])
+          return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
+        if (cudaMemsetAsync(op->ctrl[r], 0, pair_ctrl_bytes(op->chunks), st) != cudaSuccess)
+          return rt_fail(AXONN_ERR_CUDA, "loopback: memset failed");
+      }
+    }
     if (op->mode == kScatter || op->mode == kExchange) {
       // scatter: P slots of elems / P; exchange: P slots of elems (whole partials)
       const int64_t rbytes = op->elems * op->es * (op->mode == kExchange ? op->P : 1);
@@ -369,6 +392,24 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     if (op.mode == kMcRed) {
       EpiTarget t = epi_red(mc_of(op, r));
       if (!real_mc) t.mode = kRedLocal;
+      return t;
+    }
+    if (op.mode == kPairSum) {  // as fused_bind in axonn.cpp: rank 0's tickets are shared
+      const std::vector<int> mem = members(r, op.axis);
+      const int me = cc[r][op.axis], peer = mem[1 - me];
+      EpiTarget t;
+      t.mode = kPairSum;
+      t.P = 2;
+      t.me = me;
+      t.slice = (op.cols + 63) / 64;
+      t.mc = reinterpret_cast<unsigned long long>(op.ctrl[mem[0]]);
+      const size_t done = pair_done_off(op.chunks);
+      t.peer[0] = reinterpret_cast<unsigned long long>(op.recv[r]);
+      t.peer[1] = reinterpret_cast<unsigned long long>(op.recv[peer]);
+      t.peer[2] = reinterpret_cast<unsigned long long>(op.out[r]);
+      t.peer[3] = reinterpret_cast<unsigned long long>(op.out[peer]);
+      t.peer[4] = reinterpret_cast<unsigned long long>(op.ctrl[r] + done);
+      t.peer[5] = reinterpret_cast<unsigned long long>(op.ctrl[peer] + done);
       return t;
     }
     if (op.mode == kScatter || op.mode == kExchange) {
@@ -409,6 +450,15 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   // every rank's owner phase (scatter mode) or local sum (exchange mode);
   // act_z: the forward GeLU rides on the exchange's local sum (Z -> act_z[r])
   auto owner_phase = [&](const LbOp& op, const std::vector<void*>* act_z = nullptr) -> axonn_status_t {
+    if (op.mode == kPairSum) {  // the epilogues finished the sums: each rank's completion wait
+      for (int r = 0; r < G; ++r) {
+        if (sym_pair_wait(op.ctrl[r] + pair_done_off(op.chunks), op.ctrl[r] + pair_calls_off(op.chunks),
+                          static_cast<uint32_t>(op.chunks), st) != cudaSuccess)
+          return rt_fail(AXONN_ERR_CUDA, "loopback: pair-sum wait launch failed");
+        rt_count_launch();
+      }
+      return AXONN_OK;
+    }
     if (op.mode == kExchange) {  // every rank sums its own P slots locally
       for (int r = 0; r < G; ++r) {
         OwnerOut o;
@@ -437,8 +487,10 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   };
   // the reduced result of rank r -> its caller buffer
   auto deliver = [&](const LbOp& op, int r, void* dst) -> axonn_status_t {
-    const char* src = ((op.mode == kScatter || op.mode == kExchange) && op.P == 2) ? op.out[r]
-                                                                                    : uc_of(op, r);
+    const char* src =
+        ((op.mode == kScatter || op.mode == kExchange || op.mode == kPairSum) && op.P == 2)
+            ? op.out[r]
+            : uc_of(op, r);
     if (op.elems &&
         cudaMemcpyAsync(dst, src, op.elems * op.es, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return rt_fail(AXONN_ERR_CUDA, "loopback: copy failed");
@@ -485,7 +537,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
 
   // ------------------------------------------------ lines 3-4: Ô, AR (Eq. 3)
   if ((s = zero_regions(fo)) != AXONN_OK) return s;
-  for (int r = 0; r < G; ++r) {
+  for (int rr = 0; rr < G; ++rr) {
+    const int r = reverse ? G - 1 - rr : rr;
     const EpiTarget t = target(fo, r);
     if ((s = rt_gemm(AXONN_OP_NN, AXONN_BF16, m_l, n_l, k_l, I[r], k_l, Wfull[r], n_l,
                      fo.mode == kStore ? O[r] : nullptr, n_l, st,
@@ -496,6 +549,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   if ((s = owner_phase(fo, act_fused ? &zbuf : nullptr)) != AXONN_OK) return s;
   if (fo.mode != kStore) {
     p |= fo.mode == kMcRed ? AXONN_LB_PATH_FWD_RED
+         : fo.mode == kPairSum ? AXONN_LB_PATH_FWD_PAIRSUM
          : fo.mode == kExchange ? AXONN_LB_PATH_FWD_EXCHANGE : AXONN_LB_PATH_FWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fo, r, O[r])) != AXONN_OK) return s;
@@ -520,7 +574,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
 
   // ------------------------------------------------ lines 11-12: dÎ, AR (Eq. 4)
   if ((s = zero_regions(fi)) != AXONN_OK) return s;
-  for (int r = 0; r < G; ++r) {
+  for (int rr = 0; rr < G; ++rr) {
+    const int r = reverse ? G - 1 - rr : rr;
     const EpiTarget t = target(fi, r);
     if ((s = rt_gemm(AXONN_OP_NT, AXONN_BF16, m_l, k_l, n_l, dOa[r], n_l, Wfull[r], n_l,
                      fi.mode == kStore ? dI[r] : nullptr, k_l, st,
@@ -530,6 +585,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   if ((s = owner_phase(fi)) != AXONN_OK) return s;
   if (fi.mode != kStore) {
     p |= fi.mode == kMcRed ? AXONN_LB_PATH_BWD_RED
+         : fi.mode == kPairSum ? AXONN_LB_PATH_BWD_PAIRSUM
          : fi.mode == kExchange ? AXONN_LB_PATH_BWD_EXCHANGE : AXONN_LB_PATH_BWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fi, r, dI[r])) != AXONN_OK) return s;
@@ -537,7 +593,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
 
   // ------------------------------------------------ line 13: dW partial
   if ((s = zero_regions(fw)) != AXONN_OK) return s;
-  for (int r = 0; r < G; ++r) {
+  for (int rr = 0; rr < G; ++rr) {
+    const int r = reverse ? G - 1 - rr : rr;
     EpiTarget t;
     const EpiTarget* tp = nullptr;
     if (fz.mode == kScatter) {
@@ -578,6 +635,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   if (fw.mode != kStore) {
     if ((s = owner_phase(fw)) != AXONN_OK) return s;
     p |= fw.mode == kMcRed ? AXONN_LB_PATH_DP_RED
+         : fw.mode == kPairSum ? AXONN_LB_PATH_DP_PAIRSUM
          : fw.mode == kExchange ? AXONN_LB_PATH_DP_EXCHANGE : AXONN_LB_PATH_DP_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fw, r, dW[r])) != AXONN_OK) return s;

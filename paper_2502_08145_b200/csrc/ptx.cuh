@@ -310,6 +310,34 @@ __device__ __forceinline__ void red_add_bf16x8(uint64_t addr, uint4 v) {
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+// System-scope atomics on local or NVLink-peer (LSA) addresses (kPairSum).
+__device__ __forceinline__ uint32_t atom_add_acqrel_sys(uint64_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release_sys(uint64_t addr, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Sum two vectors of 8 bf16 in fp32, one RNE rounding (R19).
+__device__ __forceinline__ uint4 add_bf16x8(uint4 a, uint4 b) {
+  const uint32_t x[4] = {a.x, a.y, a.z, a.w}, y[4] = {b.x, b.y, b.z, b.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float lo = __uint_as_float(x[q] << 16) + __uint_as_float(y[q] << 16);
+    const float hi = __uint_as_float(x[q] & 0xFFFF0000u) + __uint_as_float(y[q] & 0xFFFF0000u);
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    o[q] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
   __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo_f32), __uint_as_float(hi_f32));
   return *reinterpret_cast<uint32_t*>(&h);

@@ -151,6 +151,25 @@ __global__ void k_gather_pull(PullSrc src, int P, long long n16, uint4* __restri
   }
 }
 
+// kPairSum completion (gemm.h): wait until every chunk of this call has been
+// finalised — by this rank's epilogue or the peer's — then advance the call
+// count.  A bounded spin: a lost chunk traps (a launch error) instead of
+// hanging the device.
+__global__ void k_pair_wait(const uint32_t* done, uint32_t* calls, uint32_t total) {
+  if (threadIdx.x != 0) return;
+  const uint32_t c = *calls;
+  const uint32_t target = (c + 1u) * total;
+  long long spins = 0;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if (static_cast<int32_t>(v - target) >= 0) break;
+    __nanosleep(256);
+    if (++spins > (1LL << 27)) __trap();
+  }
+  *calls = c + 1u;
+}
+
 __global__ void k_barrier(ncclDevComm dc, uint32_t index, int* ctr) {
   ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), index);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
@@ -336,12 +355,14 @@ cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* d
 }
 
 int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
-               bool exchange2) {
+               bool exchange2, bool pairsum2) {
   const int64_t n = rows * cols;
   const int unit = 16 / es;  // elements per 16-B epilogue unit
   // not fused: a 1-rank axis, an empty output, rows not a whole number of
   // 16-B units, or an empty product (K == 0 writes zeros; nothing to scatter)
   if (P < 2 || n <= 0 || cols % unit || kdim <= 0) return kStore;
+  // 2-rank bf16: the sum finished inside the epilogue (no post pass, no barrier)
+  if (es == 2 && P == 2 && pairsum2) return kPairSum;
   // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
   if (es == 2 && P == 2 && kdim >= red_min_k) return kMcRed;
   // 2-rank axes: exchange whole partials, then sum locally (no owner broadcast)
@@ -393,6 +414,12 @@ cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* d
   if (blocks < 1) blocks = 1;
   k_gather_pull<<<static_cast<unsigned>(blocks), 256, 0, st>>>(ps, P, n16,
                                                                static_cast<uint4*>(dst));
+  return cudaGetLastError();
+}
+
+cudaError_t sym_pair_wait(const void* done, void* calls, uint32_t total, cudaStream_t st) {
+  k_pair_wait<<<1, 32, 0, st>>>(static_cast<const uint32_t*>(done), static_cast<uint32_t*>(calls),
+                                total);
   return cudaGetLastError();
 }
 

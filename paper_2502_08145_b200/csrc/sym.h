@@ -97,7 +97,15 @@ cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0, int* ctr = n
 // P == 1).  2-rank bf16 axes use multimem.red when kdim >= red_min_k, else
 // (exchange2) the exchange of whole partials, else the scatter + owner phase.
 int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
-               bool exchange2);
+               bool exchange2, bool pairsum2);
+// kPairSum: the control block of a pair-sum reduction (per rank, symmetric):
+// [0, 4*chunks) arbitration tickets (rank 0's copy is the shared one),
+// then the done counter and the call counter.
+inline size_t pair_ctrl_bytes(long long chunks) { return static_cast<size_t>(chunks) * 4 + 256; }
+inline size_t pair_done_off(long long chunks) { return static_cast<size_t>(chunks) * 4 + 128; }
+inline size_t pair_calls_off(long long chunks) { return static_cast<size_t>(chunks) * 4 + 192; }
+// Wait until *done reaches (*calls + 1) * total, then advance *calls (one thread).
+cudaError_t sym_pair_wait(const void* done, void* calls, uint32_t total, cudaStream_t st);
 // Epilogue targets: multimem.red into `mc`; scatter of 16-B units to the
 // owners' receive slots peer[0..P) (owner o = flat / slice).
 EpiTarget epi_red(unsigned long long mc);

@@ -137,9 +137,11 @@ def _expected_paths(cfg, transposed, flags, grad_f32=False):
     forced, or scatter + owner phase when exchange is off), wider axes scatter."""
     ax_f, ax_b = (0, 1) if transposed else (1, 0)
     want = set()
-    red2, no_x = bool(flags & 1), bool(flags & 16)
+    red2, no_x, pair = bool(flags & 1), bool(flags & 16), bool(flags & 32)
 
     def two(name, es2=True):
+        if pair and es2:
+            return f"{name}_pairsum"
         return f"{name}_red" if (red2 and es2) else (f"{name}_scatter" if no_x else f"{name}_exchange")
     for name, P in (("fwd", cfg[ax_f]), ("bwd", cfg[ax_b])):
         if P == 2:
@@ -203,6 +205,10 @@ def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
     check(ax, G, cfg, transposed, "int", 0)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE)
+    # the sum finished inside the epilogue (kPairSum), each rank of a pair in
+    # both roles (the second arriver sums and writes both outputs)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM | ax.AXONN_LB_REVERSE)
 
 
 @pytest.mark.parametrize("transposed", [False, True])
@@ -341,7 +347,7 @@ def check_act(ax, G, cfg, transposed, flags=0):
     The oracle: alg1.simulate gives each rank's Z; the backward is simulated
     with the global dZ = dY ⊙ GELU'(X W) (oracle.act)."""
     from oracle import act
-    m, k, n = SHAPES[G]
+    m, k, n = SHAPES.get(G, SHAPES[2])
     (X, W, dY), outs, paths = run_loopback_act(ax, m, k, n, cfg, transposed, flags)
     Zg = fc.fc_forward(X, W)
     dZ = dY * act.gelu_grad(Zg)

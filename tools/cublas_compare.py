@@ -27,6 +27,11 @@ def main():
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--once", action="store_true", help="1 warm-up + 1 step of each (for ncu)")
+    ap.add_argument("--cool", type=float, default=0.0,
+                    help="idle seconds before each timed window (short windows then start from "
+                         "a rested power state, as a fresh bench run does)")
+    ap.add_argument("--per-op", action="store_true",
+                    help="also time each of the 12 products separately (CUDA events per launch)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     bf = torch.bfloat16
@@ -60,7 +65,52 @@ def main():
 
     flops = model_flops(layers)
 
+    def ops_axonn():
+        out = []
+        for t in T:
+            m, k, n = t["mkn"]
+            out.append((f"fwd NN {m}x{n}x{k}", 2 * m * n * k,
+                        lambda t=t, m=m, k=k, n=n: ax.axonn_gemm(0, 0, m, n, k, t["I"], k, t["W"], n, t["O"], n, s)))
+        for t in reversed(T):
+            m, k, n = t["mkn"]
+            out.append((f"dI NT {m}x{k}x{n}", 2 * m * n * k,
+                        lambda t=t, m=m, k=k, n=n: ax.axonn_gemm(1, 0, m, k, n, t["dO"], n, t["W"], n, t["dI"], k, s)))
+            out.append((f"dW TN {k}x{n}x{m}", 2 * m * n * k,
+                        lambda t=t, m=m, k=k, n=n: ax.axonn_gemm(2, 0, k, n, m, t["I"], k, t["dO"], n, t["dW"], n, s)))
+        return out
+
+    def ops_cublas():
+        out = []
+        for t in T:
+            m, k, n = t["mkn"]
+            out.append((f"fwd NN {m}x{n}x{k}", 2 * m * n * k,
+                        lambda t=t: torch.matmul(t["I"], t["W"], out=t["O"])))
+        for t in reversed(T):
+            m, k, n = t["mkn"]
+            out.append((f"dI NT {m}x{k}x{n}", 2 * m * n * k,
+                        lambda t=t: torch.matmul(t["dO"], t["W"].t(), out=t["dI"])))
+            out.append((f"dW TN {k}x{n}x{m}", 2 * m * n * k,
+                        lambda t=t: torch.matmul(t["I"].t(), t["dO"], out=t["dW"])))
+        return out
+
+    def per_op(ops, steps):
+        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in ops] for _ in range(steps)]
+        with torch.cuda.stream(s):
+            for st in range(steps):
+                for (name, fl, fn), (a, b) in zip(ops, evs[st]):
+                    a.record(s)
+                    fn()
+                    b.record(s)
+        torch.cuda.synchronize()
+        return [(name, fl / (sum(evs[st][i][0].elapsed_time(evs[st][i][1]) for st in range(steps)) / steps * 1e-3) / 1e12)
+                for i, (name, fl, _) in enumerate(ops)]
+
     def timed(fn):
+        import time as _t
+        if args.cool > 0:
+            torch.cuda.synchronize()
+            _t.sleep(args.cool)
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -93,6 +143,17 @@ def main():
     a = max(res["axonn"])
     c = max(res["cublas"])
     print(f"best: axonn {a:.1f} TFLOP/s, cublas {c:.1f} TFLOP/s, ratio {a / c:.3f}")
+    if args.per_op:
+        import time as _t
+        for name, ops in (("axonn", ops_axonn()), ("cublas", ops_cublas())):
+            torch.cuda.synchronize()
+            if args.cool > 0:
+                _t.sleep(args.cool)
+            for _, _, fn in ops:
+                fn()
+            r = per_op(ops, 3)
+            for op, tf in r:
+                print(f"per-op {name:7s} {op:28s} {tf:8.1f} TFLOP/s", flush=True)
 
 
 if __name__ == "__main__":

@@ -31,7 +31,9 @@ sys.path.insert(0, ROOT)
 
 import paper_2502_08145_b200 as ax  # noqa: E402
 
-TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX (KiB)
+# (tx, rx, bytes per unit): NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/_RX (KiB),
+# NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES (bytes), tried in order
+FIELDS = [(138, 139, 1024), (202, 204, 1)]
 
 
 def nvml_handle(local):
@@ -42,21 +44,31 @@ def nvml_handle(local):
         f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
 
 
+_FIELD = None
+
+
 def counters(h, nlinks=18):
-    """(tx, rx) bytes summed over links; None if the fields are unavailable."""
+    """(tx, rx) bytes summed over links (or the device total); None if no field
+    is available.  The first field set and scope that answers is kept."""
     import pynvml
-    tot = [0, 0]
-    ok = False
-    for link in range(nlinks):
-        try:
-            vals = pynvml.nvmlDeviceGetFieldValues(h, [(TX, link), (RX, link)])
-        except Exception:
-            continue
-        for i, v in enumerate(vals):
-            if v.nvmlReturn == 0:
-                ok = True
-                tot[i] += int(v.value.ullVal) * 1024
-    return tuple(tot) if ok else None
+    global _FIELD
+    cands = [_FIELD] if _FIELD else [(f, sc) for f in FIELDS for sc in ("links", "all")]
+    for (tx, rx, unit), scope in cands:
+        scopes = range(nlinks) if scope == "links" else [0xFFFFFFFF]
+        tot, ok = [0, 0], False
+        for link in scopes:
+            try:
+                vals = pynvml.nvmlDeviceGetFieldValues(h, [(tx, link), (rx, link)])
+            except Exception:
+                continue
+            for i, v in enumerate(vals):
+                if v.nvmlReturn == 0:
+                    ok = True
+                    tot[i] += int(v.value.ullVal) * unit
+        if ok:
+            _FIELD = ((tx, rx, unit), scope)
+            return tuple(tot)
+    return None
 
 
 def main():
@@ -107,6 +119,10 @@ def main():
             call()
         torch.cuda.synchronize()
         dist.barrier()
+        # align the two GPUs' starts (a device-side collective right before the timed calls)
+        z = torch.zeros(1, device="cuda")
+        with torch.cuda.stream(s):
+            dist.all_reduce(z)
         # the forward alone, to subtract from "bwd" sites (its collective may be idle there)
         ax.axonn_comm_bytes(reset=True)
         c0 = counters(nv)
@@ -121,6 +137,7 @@ def main():
         eq = ax.axonn_comm_bytes(reset=True)
         eq = {k: v // args.iters for k, v in eq.items()}
         rec = {"site": name, "grid": list(cfg), "layer": [m, k, n, t], "rank": rank,
+               "field": str(_FIELD),
                "ms_per_call": ms, "eqs_1_5_bytes_per_call": eq,
                "fused_axes": {a: ax.axonn_fused_status(a) for a in "xyzd"}}
         if c0 and c1:
