@@ -272,8 +272,11 @@ enum {
   AXONN_LB_NO_EXCHANGE = 16, /* 2-rank axes below the red threshold: scatter +
                                 owner phase instead of the exchange of partials */
   AXONN_LB_PAIRSUM = 32,     /* 2-rank bf16 axes: the sum finished in the epilogue */
-  AXONN_LB_REVERSE = 64      /* run each phase's ranks in reverse order (the
+  AXONN_LB_REVERSE = 64,     /* run each phase's ranks in reverse order (the
                                 pair-sum's second arriver is then rank 0)     */
+  AXONN_LB_PAIRPULL = 128    /* with AXONN_LB_PAIRSUM: each rank keeps its partial
+                                in its own receive buffer and the second
+                                arriver reads the peer's over NVLink (pull)   */
 };
 enum {
   AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,
@@ -306,6 +309,11 @@ axonn_status_t axonn_profile_read(int64_t* gemm_launches, double* gemm_ms, doubl
 /* Kernels launched by this library since load (GEMMs + helper kernels; NCCL
  * kernels excluded). */
 int64_t axonn_kernel_launches(void);
+/* GEMM launches since load that split their last, partial wave of tiles along
+ * K (the stream-K tail of gemm_tc.cu: tiles that would leave CTA pairs idle
+ * are shared by all pairs; a tile's two pieces are summed in fp32 in a fixed
+ * order, so results are deterministic).  AXONN_SK=0 turns the split off. */
+int64_t axonn_stream_k_launches(void);
 /* SM budget of the persistent GEMM grid (<= 0 or > #SMs: all SMs).  Leaving
  * SMs free lets NCCL kernels run beside the GEMM when collectives overlap. */
 axonn_status_t axonn_set_gemm_sms(int sms);

@@ -32,7 +32,7 @@ AXONN_OP_NN, AXONN_OP_NT, AXONN_OP_TN = 0, 1, 2
 AXONN_ACT_NONE, AXONN_ACT_GELU = 0, 1
 AXIS = {"x": 0, "y": 1, "z": 2, "d": 3}
 AXONN_LB_RED_ALWAYS, AXONN_LB_RED_NEVER, AXONN_LB_GATHER_PULL, AXONN_LB_EMULATE_MC = 1, 2, 4, 8
-AXONN_LB_NO_EXCHANGE, AXONN_LB_PAIRSUM, AXONN_LB_REVERSE = 16, 32, 64
+AXONN_LB_NO_EXCHANGE, AXONN_LB_PAIRSUM, AXONN_LB_REVERSE, AXONN_LB_PAIRPULL = 16, 32, 64, 128
 LB_PATHS = {"fwd_red": 1, "fwd_scatter": 2, "bwd_red": 4, "bwd_scatter": 8, "rs_z": 16,
             "dp_red": 32, "dp_scatter": 64, "dp_after_rs": 128, "gather_copy": 256,
             "gather_pull": 512, "multicast": 1024, "fwd_exchange": 2048, "bwd_exchange": 4096,
@@ -108,6 +108,7 @@ _PROTOS = {
     "axonn_profile_enable": (_S, [c_int]),
     "axonn_profile_read": (_S, [POINTER(c_int64), POINTER(c_double), POINTER(c_double)]),
     "axonn_kernel_launches": (c_int64, []),
+    "axonn_stream_k_launches": (c_int64, []),
     "axonn_set_gemm_sms": (_S, [c_int]),
     "axonn_comm_bytes": (_S, [POINTER(c_int64), c_int]),
     "axonn_grid_select": (_S, [POINTER(LayerT), c_int, c_int, c_int, POINTER(BwEntry), c_int,
@@ -298,6 +299,10 @@ def axonn_profile_read():
 
 def axonn_kernel_launches() -> int:
     return _lib.axonn_kernel_launches()
+
+
+def axonn_stream_k_launches() -> int:
+    return _lib.axonn_stream_k_launches()
 
 
 def axonn_set_gemm_sms(sms: int) -> None:

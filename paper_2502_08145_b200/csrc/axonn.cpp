@@ -448,8 +448,14 @@ bool fused_bind(axonn_fc::Fused* f, std::string* why) {
     t.slice = (f->cols + 63) / 64;
     t.mc = reinterpret_cast<unsigned long long>(arb);
     const size_t done = axonn::pair_done_off(f->chunks);
-    t.peer[0] = reinterpret_cast<unsigned long long>(f->recv.ptr);
-    t.peer[1] = reinterpret_cast<unsigned long long>(precv);
+    // AXONN_PAIRSUM=1 push: our partial goes to the peer's receive buffer
+    // (peer[1]) and the second arriver reads the peer's from ours (peer[0]);
+    // =2 pull: our partial stays in our own buffer and the second arriver
+    // reads the peer's over NVLink from the peer's buffer — per rank half the
+    // NVLink bytes of push on average (the first arriver sends nothing)
+    const bool pull = env_int("AXONN_PAIRSUM", 0) == 2;
+    t.peer[0] = reinterpret_cast<unsigned long long>(pull ? static_cast<void*>(precv) : f->recv.ptr);
+    t.peer[1] = reinterpret_cast<unsigned long long>(pull ? f->recv.ptr : static_cast<void*>(precv));
     t.peer[2] = reinterpret_cast<unsigned long long>(f->out.ptr);
     t.peer[3] = reinterpret_cast<unsigned long long>(pout);
     t.peer[4] = reinterpret_cast<unsigned long long>(static_cast<char*>(f->ctrl.ptr) + done);
@@ -1336,6 +1342,11 @@ axonn_status_t axonn_profile_read(int64_t* launches, double* ms, double* flops) 
 }
 
 int64_t axonn_kernel_launches(void) { return g_launches.load(); }
+
+int64_t axonn_stream_k_launches(void) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  return axonn::gemm_stream_k_launches();
+}
 
 axonn_status_t axonn_comm_bytes(int64_t out[5], int reset) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);

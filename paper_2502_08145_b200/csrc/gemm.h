@@ -55,6 +55,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
 // The launch error behind the last GemmStatus::kLaunch on this thread (the
 // launch helpers consume cudaGetLastError()).
 cudaError_t gemm_last_launch_error();
+// launches that used the stream-K tail (axonn_stream_k_launches)
+long long gemm_stream_k_launches();
 
 // fp32 SIMT FMA (test mode, no TF32): same op codes.
 GemmStatus gemm_f32_simt(int op, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

@@ -263,35 +263,119 @@ __global__ void __launch_bounds__(THREADS, 1)
 //           TMEM columns: 33% more flops per byte staged from L2 and a quarter
 //           fewer operand-panel reads per GEMM, which lowers L2/DRAM traffic
 //           and power (the B200 runs power-capped under this load).
-template <int MT>
+template <int MT, int DEEP = 0>
 struct PairCfg {
   static constexpr int ROWS_CTA = 128 * MT;
   static constexpr int BM = 256 * MT;
   static constexpr int BN = 256;
-  static constexpr int STAGES = MT == 1 ? 5 : 3;
+  // DEEP (MT = 2 only): a 4th operand stage in place of the second epilogue
+  // staging box, so the next tile's first 4 K-blocks (not 3) accumulate into
+  // sub-tile 0 while the epilogue still drains sub-tile 1
+  static constexpr int STAGES = MT == 1 ? 5 : (DEEP ? 4 : 3);
   static constexpr int ACC = 2 / MT;                // accumulator buffers in TMEM
   static constexpr int SMEM_A = ROWS_CTA * BK * 2;
   static constexpr int SMEM_B = 128 * BK * 2;
   static constexpr int STAGE_BYTES = SMEM_A + SMEM_B;
   static constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each owning half the columns
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  // per warp: two 32 x 64 bf16 staging boxes (the TMA store of one overlaps filling the other)
-  static constexpr int EPI_BYTES = EPI_WARPS * 2 * 32 * 64 * 2;
+  // per warp: 32 x 64 bf16 staging boxes; with two, the TMA store of one overlaps filling the other
+  static constexpr int EPI_BOXES = DEEP ? 1 : 2;
+  static constexpr int EPI_BYTES = EPI_WARPS * EPI_BOXES * 32 * 64 * 2;
   static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+  static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
+
+// ------------------------------------------------------------ stream-K tail
+// When a launch's tiles do not fill whole waves of CTA pairs (e.g. the C2 proj
+// dW: 128 tiles of 512x256 over 74 pairs, 1.73 waves), the first
+// `sk_tiles` = (tiles mod pairs) + pairs tiles in raster order are split along K:
+// their sk_tiles x num_kb K-blocks are dealt out evenly, pair c taking the
+// contiguous range [u0, u1) (at least one tile's worth, so a tile has at most
+// two pieces).  Pair c processes, in order: the HEAD of the tile its range
+// ends in (K-blocks [0, h): the contributor, fp32 partial sums to a
+// workspace), the whole tiles inside its range, and the TAIL of the tile its
+// range starts in (K-blocks [t0, num_kb): the finisher, which adds pair c-1's
+// partial sums before the epilogue proper).  Every pair then draws the
+// remaining tiles (whole waves) from the dynamic tile counter.
+//
+// No pair ever waits on a pair that has not started: the contributor claims
+// its HEAD (claim 0 -> 1) when its producer reaches it (its first item); a
+// finisher that finds the claim still 0 takes the whole tile itself (0 -> 2,
+// role WHOLE) and the contributor, seeing 2, skips its HEAD and resets the
+// claim.  A finisher therefore only waits on a running pair, so a grid that
+// is not fully resident still completes.  Claims and ready flags return to 0
+// by the end of every launch.  The sums are deterministic: fixed split points
+// and one fixed addition order (partial of K-blocks [0, t0) + the rest).
+struct SkParams {
+  int sk_tiles = 0;         // tiles [0, sk_tiles) split along K; 0 = off
+  int units = 0;            // sk_tiles * num_kb
+  float4* ws = nullptr;     // per SK tile: 2 CTAs x MT x 8 warps x 4 x 8 x 32 float4
+  int* claim = nullptr;     // per SK tile
+  int* ready = nullptr;     // per SK tile x 2 CTAs x 8 epilogue warps
+};
+
+enum : int { kRoleFull = 0, kRoleHead = 1, kRoleTail = 2, kRoleWhole = 3 };
+
+__device__ __forceinline__ int item_tile(int it) { return it & 0x0FFFFFFF; }
+__device__ __forceinline__ int item_role(int it) { return static_cast<int>(static_cast<unsigned>(it) >> 28); }
+__device__ __forceinline__ int make_item(int tile, int role) { return tile | (role << 28); }
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ float4 ld_cg_f4(const float4* p) {  // L2 only: written by another SM
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t addf(uint32_t a, float b) {
+  return __float_as_uint(__uint_as_float(a) + b);
+}
+
+// the idx-th stream-K item of the pair owning K-block range [u0, u1)
+// (HEAD, whole tiles, TAIL), or -1 past the end
+__device__ __forceinline__ int sk_static_item(int u0, int u1, int kb, int idx) {
+  int n = 0;
+  if (u1 % kb) {
+    if (idx == n) return make_item(u1 / kb, kRoleHead);
+    ++n;
+  }
+  const int f0 = (u0 + kb - 1) / kb, f1 = u1 / kb;
+  if (f1 > f0) {
+    if (idx < n + (f1 - f0)) return make_item(f0 + idx - n, kRoleFull);
+    n += f1 - f0;
+  }
+  if (u0 % kb) {
+    if (idx == n) return make_item(u0 / kb, kRoleTail);
+  }
+  return -1;
+}
+
+// K-block range of an item for the pair owning [u0, u1)
+__device__ __forceinline__ void item_kb(int it, int u0, int u1, int kb, int* kb0, int* kb1) {
+  const int t = item_tile(it), r = item_role(it);
+  *kb0 = r == kRoleTail ? u0 - t * kb : 0;
+  *kb1 = r == kRoleHead ? u1 - t * kb : kb;
+}
 
 // OUTF = 1: fp32 output (the dW GEMM when gradients are reduced in fp32,
 // SURVEY.md §8(f) f-4): the accumulator is stored without rounding.
-template <int A_MN, int B_MN, int MT, int OUTF>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS, 1)
+template <int A_MN, int B_MN, int MT, int OUTF, int DEEP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::THREADS, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmC, int use_tma_store,
                            void* __restrict__ Cv, int64_t ldc, int M, int N, int K,
                            int split_release,
                            int group_m, const __grid_constant__ EpiTarget epi,
-                           int* __restrict__ tile_counter) {
-  using Cfg = PairCfg<MT>;
+                           int* __restrict__ tile_counter, const __grid_constant__ SkParams sk) {
+  using Cfg = PairCfg<MT, DEEP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -318,14 +402,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + BK - 1) / BK;
   const bool dynamic = tile_counter != nullptr;
+  // stream-K (dynamic scheduling only): this pair's K-block range
+  const bool skon = dynamic && sk.sk_tiles > 0;
+  const int sk_u0 = skon ? static_cast<int>(static_cast<long long>(sk.units) * cluster / nclusters) : 0;
+  const int sk_u1 = skon ? static_cast<int>(static_cast<long long>(sk.units) * (cluster + 1) / nclusters) : 0;
 
-  // Tile sequence.  Static: cluster c takes c, c + nclusters, ...  Dynamic:
-  // the leader's producer draws the next tile in raster order from a global
-  // counter when its cluster is ready for one, and publishes it to both CTAs'
+  // Work sequence.  Static: cluster c takes tiles c, c + nclusters, ...
+  // Dynamic: the leader's producer decides the next item — its stream-K
+  // items first (above), then tiles in raster order from a global counter
+  // when its cluster is ready for one — and publishes it to both CTAs'
   // 4-entry queues; the other consumers (peer producer, MMA, every epilogue
   // warp of both CTAs) read their own copy and release the slot on the leader.
   // Keeping the tiles in flight a compact band of the raster keeps the
   // operand panels they share resident in L2 across the whole K loop.
+  // An item is a tile index with its stream-K role in bits 28..31; -1 ends.
   auto consume_tile = [&](int seq, bool arrive) -> int {
     if (!dynamic) {
       const int t = cluster + seq * nclusters;
@@ -337,6 +427,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
     if (arrive) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_empty[slot]), 0));
     return t;
   };
+  int sk_idx = 0;  // leader producer: next stream-K item of this pair
+  auto next_item = [&]() -> int {
+    while (skon) {
+      const int it = sk_static_item(sk_u0, sk_u1, num_kb, sk_idx);
+      if (it < 0) break;
+      ++sk_idx;
+      const int t = item_tile(it);
+      if (item_role(it) == kRoleHead) {
+        if (atomicCAS(&sk.claim[t], 0, 1) == 0) return it;
+        atomicExch(&sk.claim[t], 0);  // the finisher took the whole tile
+        continue;
+      }
+      if (item_role(it) == kRoleTail)
+        return atomicCAS(&sk.claim[t], 0, 2) == 0 ? make_item(t, kRoleWhole) : it;
+      return it;
+    }
+    int t = atomicAdd(tile_counter, 1) + sk.sk_tiles;
+    return t < num_tiles ? t : -1;
+  };
   auto produce_tile = [&](int seq) -> int {  // leader producer
     if (!dynamic) {
       const int t = cluster + seq * nclusters;
@@ -344,8 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
     }
     const int slot = seq & 3;
     ptx::mbar_wait_cluster(&tq_empty[slot], ((seq >> 2) & 1) ^ 1);
-    int t = atomicAdd(tile_counter, 1);
-    if (t >= num_tiles) t = -1;
+    const int t = next_item();
     tq[slot] = t;
     ptx::st_shared_cluster_u32(ptx::mapa_shared(ptx::smem_u32(&tq[slot]), 1), static_cast<uint32_t>(t));
     ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_full[slot]), 0));
@@ -383,12 +491,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
       int stage = 0;
       uint32_t phase = 0;
       for (int seq = 0;; ++seq) {
-        const int t = leader ? produce_tile(seq) : consume_tile(seq, true);
-        if (t < 0) break;
-        const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
+        const int it = leader ? produce_tile(seq) : consume_tile(seq, true);
+        if (it < 0) break;
+        int kb0, kb1;
+        item_kb(it, sk_u0, sk_u1, num_kb, &kb0, &kb1);
+        const TileCoord tc = tile_coord_g(item_tile(it), tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
         const int am = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank);  // this CTA's A rows
         const int bn = tc.n0 + 128 * static_cast<int>(rank);            // this CTA's half of N
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
           const int k0 = kb * BK;
@@ -453,7 +563,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
         }
       };
       for (int seq = 0;; ++seq) {
-        if (consume_tile(seq, true) < 0) break;
+        const int it = consume_tile(seq, true);
+        if (it < 0) break;
+        int kb0, kb1;
+        item_kb(it, sk_u0, sk_u1, num_kb, &kb0, &kb1);
+        const int nkb = kb1 - kb0;  // K-blocks of this item (kb below counts from 0)
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * MT * Cfg::BN);
         int kb = 0;
         if (MT == 2) {
@@ -463,7 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           ptx::mbar_wait(&tempty[0], acc_phase ^ 1);
           if (!split_release) ptx::mbar_wait(&tempty[1], acc_phase ^ 1);
           ptx::tc_fence_after();
-          const int pro = !split_release ? 0 : num_kb < Cfg::STAGES ? num_kb : Cfg::STAGES;
+          const int pro = !split_release ? 0 : nkb < Cfg::STAGES ? nkb : Cfg::STAGES;
           int st2 = stage;
           uint32_t ph2 = phase;
           for (int j = 0; j < pro; ++j) {
@@ -485,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
           ptx::tc_fence_after();
         }
-        for (; kb < num_kb; ++kb) {
+        for (; kb < nkb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           issue(d_tmem, stage, kb, 0, MT);
@@ -518,7 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
     uint32_t acc_phase = 0;
     const bool vec_ok =
         ((ldc * ELEM) % 16 == 0) && ((reinterpret_cast<uintptr_t>(Cv) & 15) == 0);
-    uint8_t* stage_base = sEpi + ew * (2 * 32 * 64 * 2);
+    uint8_t* stage_base = sEpi + ew * (Cfg::EPI_BOXES * 32 * 64 * 2);
     // kExchange double buffering: the receive buffers of this call (parity
     // counter written in stream order by the previous call's barrier kernel)
     const unsigned long long* xbase =
@@ -532,29 +646,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
       if (dynamic && lane == 0)
         ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_empty[seq & 3]), 0));
       if (t < 0) break;
-      const TileCoord tc = tile_coord_g(t, tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
+      const int role = item_role(t);
+      const TileCoord tc = tile_coord_g(item_tile(t), tiles_m, tiles_n, group_m, Cfg::BM, Cfg::BN);
+      // stream-K: this warp's workspace units (32 lanes x 16 B, coalesced) and ready flag
+      const size_t ws_warp = ((static_cast<size_t>(item_tile(t)) * 2 + rank) * MT * 8 + ew) * (4 * 8 * 32) + lane;
+      auto ws_unit = [&](int mt, int q, int j) -> float4* {
+        return sk.ws + ws_warp + static_cast<size_t>(mt) * (8 * 4 * 8 * 32) + (q * 8 + j) * 32;
+      };
+      int* const ready = sk.ready + (item_tile(t) * 2 + static_cast<int>(rank)) * 8 + ew;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      if (role == kRoleTail) {  // the contributor's partial sums have landed
+        if (lane == 0)
+          while (ld_acquire_gpu(ready) == 0) __nanosleep(100);
+        __syncwarp();
+      }
 #pragma unroll 1
       for (int mt = 0; mt < MT; ++mt) {
         const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
         const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
+        if (role == kRoleHead) {
+          // contributor: fp32 partial sums of K-blocks [0, h) to the workspace
 #pragma unroll 1
-        for (int c = chalf * NCH; c < chalf * NCH + NCH; ++c) {
+          for (int q = 0; q < 4; ++q) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
+                                        static_cast<uint32_t>(chalf * 128 + q * 32),
+                                    v);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *ws_unit(mt, q, j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0 && (MT == 2 || mt == MT - 1)) ptx::mbar_arrive_leader(&tempty[MT == 2 ? mt : acc]);
+          continue;
+        }
+        // bf16: this warp's share of sub-tile mt goes TMEM -> registers (RNE-packed)
+        // first and the sub-tile is released at once, so the MMA warp resumes
+        // before the staging and stores below
+        uint32_t pk[OUTF ? 1 : NCH][32];
+        if constexpr (!OUTF) {
+#pragma unroll
+          for (int ci = 0; ci < NCH; ++ci) {
+            uint32_t v0[32], v1[32];
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
+                                   static_cast<uint32_t>((chalf * NCH + ci) * CCOLS);
+            ptx::tmem_ld_32x32b_x32(taddr, v0);
+            ptx::tmem_ld_32x32b_x32(taddr + 32, v1);
+            ptx::tmem_wait_ld();
+            if (role == kRoleTail) {  // finisher: + the partial sums of K-blocks [0, t0)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 w0 = ld_cg_f4(ws_unit(mt, 2 * ci, j));
+                const float4 w1 = ld_cg_f4(ws_unit(mt, 2 * ci + 1, j));
+                v0[4 * j] = addf(v0[4 * j], w0.x);
+                v0[4 * j + 1] = addf(v0[4 * j + 1], w0.y);
+                v0[4 * j + 2] = addf(v0[4 * j + 2], w0.z);
+                v0[4 * j + 3] = addf(v0[4 * j + 3], w0.w);
+                v1[4 * j] = addf(v1[4 * j], w1.x);
+                v1[4 * j + 1] = addf(v1[4 * j + 1], w1.y);
+                v1[4 * j + 2] = addf(v1[4 * j + 2], w1.z);
+                v1[4 * j + 3] = addf(v1[4 * j + 3], w1.w);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              pk[ci][i] = ptx::pack_bf16x2(v0[2 * i], v0[2 * i + 1]);
+              pk[ci][16 + i] = ptx::pack_bf16x2(v1[2 * i], v1[2 * i + 1]);
+            }
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_leader(&tempty[MT == 2 ? mt : acc]);
+        }
+#pragma unroll (OUTF ? 1 : NCH)
+        for (int ci = 0; ci < NCH; ++ci) {
+          const int c = chalf * NCH + ci;
           const bool tma = use_tma_store && epi.mode == kStore;
-          uint8_t* stage = stage_base + (tma ? (nstore & 1) * (32 * 64 * 2) : 0);
+          uint8_t* stage =
+              stage_base + (tma && Cfg::EPI_BOXES == 2 ? (nstore & 1) * (32 * 64 * 2) : 0);
           const uint32_t stage_u32 = ptx::smem_u32(stage);
           if (tma) {
-            // the store issued two chunks ago read this box: make sure it is done
-            if (lane == 0) ptx::tma_store_wait_read_le1();
+            // the store issued EPI_BOXES chunks ago read this box: make sure it is done
+            if (lane == 0) {
+              if (Cfg::EPI_BOXES == 2)
+                ptx::tma_store_wait_read_le1();
+              else
+                ptx::tma_store_wait_read();
+            }
             __syncwarp();
           }
-          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
-                                 static_cast<uint32_t>(c * CCOLS);
-          if (OUTF) {
+          if constexpr (OUTF) {
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
+                                   static_cast<uint32_t>(c * CCOLS);
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(taddr, v);
             ptx::tmem_wait_ld();
+            if (role == kRoleTail) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 w = ld_cg_f4(ws_unit(mt, ci, j));
+                v[4 * j] = addf(v[4 * j], w.x);
+                v[4 * j + 1] = addf(v[4 * j + 1], w.y);
+                v[4 * j + 2] = addf(v[4 * j + 2], w.z);
+                v[4 * j + 3] = addf(v[4 * j + 3], w.w);
+              }
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {  // 16-B unit = 4 fp32 columns
               const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
@@ -563,24 +763,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
                            : "memory");
             }
           } else {
-            uint32_t v0[32], v1[32];
-            ptx::tmem_ld_32x32b_x32(taddr, v0);
-            ptx::tmem_ld_32x32b_x32(taddr + 32, v1);
-            ptx::tmem_wait_ld();
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const uint32_t* v = hh ? v1 : v0;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int j = hh * 4 + q;  // 16-B unit = 8 bf16 columns
-                const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                             "r"(ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1])),
-                             "r"(ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
-                             "r"(ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5])),
-                             "r"(ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
-                             : "memory");
-              }
+            for (int j = 0; j < 8; ++j) {  // 16-B unit = 8 bf16 columns
+              const uint32_t a = stage_u32 + lane * 128 + ((j ^ (lane & 7)) << 4);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[ci][4 * j]),
+                           "r"(pk[ci][4 * j + 1]), "r"(pk[ci][4 * j + 2]), "r"(pk[ci][4 * j + 3])
+                           : "memory");
             }
           }
           if (tma) {
@@ -705,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           }
           __syncwarp();
         }
-        if (MT == 2) {
+        if (OUTF && MT == 2) {
           // this warp's share of sub-tile mt is out of TMEM: release it (the
           // MMA warp starts the next tile on sub-tile 0 before sub-tile 1 is free)
           ptx::tc_fence_before();
@@ -713,7 +901,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT>::THREADS
           if (lane == 0) ptx::mbar_arrive_leader(&tempty[mt]);
         }
       }
-      if (MT != 2) {
+      if (role == kRoleHead) {
+        // every lane's partial sums are written before the flag is raised
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(ready, 1);
+      } else if (role == kRoleTail && lane == 0) {
+        *ready = 0;  // back to 0 for the next launch (the only reader is done)
+        if (rank == 0 && ew == 0) sk.claim[item_tile(t)] = 0;
+      }
+      if (OUTF && MT != 2 && role != kRoleHead) {
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
@@ -814,12 +1011,69 @@ int* next_tile_counter(cudaStream_t stream) {
   return c;
 }
 
-template <int A_MN, int B_MN, int MT, int OUTF = 0>
+// Stream-K tail (see SkParams): split the first (tiles mod pairs) + pairs
+// tiles along K when whole-tile waves would leave more than AXONN_SK_LOSS
+// percent (default 4) of the pairs idle, the tiles fill at least one wave and
+// K is long enough to split (>= 16 K-blocks).  Workspaces come from a ring of
+// kSkSlots (zeroed once; every launch leaves its flags at 0), so launches on
+// different streams share a slot only when more than kSkSlots stream-K GEMMs
+// are in flight at once.  AXONN_SK=0 disables it.  Called under the library
+// mutex.
+long long g_sk_launches = 0;
+
+SkParams stream_k_plan(int tiles, int pairs, int num_kb, int mt, cudaStream_t stream) {
+  static const bool on = env_int("AXONN_SK", 1) != 0;
+  static const int loss_pct = env_int("AXONN_SK_LOSS", 4);
+  SkParams p;
+  if (!on || pairs < 1 || tiles < pairs || tiles % pairs == 0 || num_kb < 16) return p;
+  const int waves = (tiles + pairs - 1) / pairs;
+  if (100LL * (static_cast<long long>(waves) * pairs - tiles) <= static_cast<long long>(loss_pct) * waves * pairs)
+    return p;
+  const int sk_tiles = tiles % pairs + pairs;
+  constexpr int kSkSlots = 4;
+  constexpr int kMaxSkTiles = 160;  // > 2 x pairs on any sm_100 part (<= 160 SMs)
+  if (sk_tiles > kMaxSkTiles) return p;
+  struct Slot {
+    float4* ws = nullptr;
+    int* flags = nullptr;
+  };
+  static Slot slots[kSkSlots];
+  static int next = 0;
+  Slot& s = slots[next];
+  const size_t ws_bytes = static_cast<size_t>(kMaxSkTiles) * 2 * 2 /*MT max*/ * 8 * 4 * 8 * 32 * 16;
+  const size_t flag_bytes = static_cast<size_t>(kMaxSkTiles) * (1 + 16) * sizeof(int);
+  if (!s.ws) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return p;  // no allocation inside a capture (the eager warm-up allocates)
+    if (cudaMalloc(&s.ws, ws_bytes) != cudaSuccess) {
+      s.ws = nullptr;
+      return p;
+    }
+    if (cudaMalloc(&s.flags, flag_bytes) != cudaSuccess || cudaMemset(s.flags, 0, flag_bytes) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+      cudaFree(s.ws);
+      s.ws = nullptr;
+      return p;
+    }
+  }
+  next = (next + 1) % kSkSlots;
+  ++g_sk_launches;
+  p.sk_tiles = sk_tiles;
+  p.units = sk_tiles * num_kb;
+  p.ws = s.ws;
+  p.claim = s.flags;
+  p.ready = s.flags + kMaxSkTiles;
+  (void)mt;
+  return p;
+}
+
+template <int A_MN, int B_MN, int MT, int OUTF = 0, int DEEP = 0>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                         int use_tma_store, void* C, int64_t ldc, int M, int N, int K, int num_sms,
                         int group_m, const EpiTarget& epi, cudaStream_t stream) {
-  using Cfg = PairCfg<MT>;
-  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT, OUTF>;
+  using Cfg = PairCfg<MT, DEEP>;
+  auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT, OUTF, DEEP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -834,20 +1088,28 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   int* counter = next_tile_counter(stream);
   // MT=2: release the accumulator per sub-tile (AXONN_SPLIT_RELEASE=0: whole tile)
   static const int split = env_int("AXONN_SPLIT_RELEASE", 1) != 0;
+  const SkParams sk = counter ? stream_k_plan(tiles, grid / 2, (K + BK - 1) / BK, MT, stream)
+                              : SkParams();
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
-                                                       split, group_m, epi, counter);
+                                                       split, group_m, epi, counter, sk);
   return cudaGetLastError();
 }
 
+// MT = 2 takes the deep-pipeline configuration (4 operand stages, one
+// epilogue staging box per warp) unless AXONN_MT2_DEEP=0.
 template <int A_MN, int B_MN>
 cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb,
                            const CUtensorMap& mc, int use_tma_store, void* C, int64_t ldc, int M,
                            int N, int K, int num_sms, int group_m, const EpiTarget& epi,
                            cudaStream_t stream) {
-  return mt == 2 ? launch_pair<A_MN, B_MN, 2>(ma, mb, mc, use_tma_store, C, ldc, M, N, K, num_sms,
-                                             group_m, epi, stream)
-                 : launch_pair<A_MN, B_MN, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K, num_sms,
-                                             group_m, epi, stream);
+  static const bool deep = env_int("AXONN_MT2_DEEP", 1) != 0;
+  if (mt == 2)
+    return deep ? launch_pair<A_MN, B_MN, 2, 0, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
+                                                   num_sms, group_m, epi, stream)
+                : launch_pair<A_MN, B_MN, 2, 0, 0>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
+                                                   num_sms, group_m, epi, stream);
+  return launch_pair<A_MN, B_MN, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K, num_sms, group_m,
+                                    epi, stream);
 }
 
 int env_int(const char* name, int dflt) {
@@ -959,5 +1221,7 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
 }
 
 cudaError_t gemm_last_launch_error() { return g_launch_error; }
+
+long long gemm_stream_k_launches() { return g_sk_launches; }
 
 }  // namespace axonn

@@ -273,6 +273,10 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   bool pairsum2 = false;
   if (const char* v = std::getenv("AXONN_PAIRSUM")) pairsum2 = std::atoi(v) != 0;
   if (flags & AXONN_LB_PAIRSUM) pairsum2 = true;
+  // pull: each rank's partial stays in its own receive buffer (AXONN_PAIRSUM=2)
+  bool pairpull = false;
+  if (const char* v = std::getenv("AXONN_PAIRSUM")) pairpull = std::atoi(v) == 2;
+  if (flags & AXONN_LB_PAIRPULL) pairpull = true;
   const bool reverse = (flags & AXONN_LB_REVERSE) != 0;
   auto members = [&](int r, int axis) {
     std::vector<int> m(g[axis]);
@@ -404,8 +408,10 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       t.slice = (op.cols + 63) / 64;
       t.mc = reinterpret_cast<unsigned long long>(op.ctrl[mem[0]]);
       const size_t done = pair_done_off(op.chunks);
-      t.peer[0] = reinterpret_cast<unsigned long long>(op.recv[r]);
-      t.peer[1] = reinterpret_cast<unsigned long long>(op.recv[peer]);
+      // push: our partial to the peer's receive buffer, the peer's read from
+      // ours; pull: ours stays in our buffer, the peer's is read from its own
+      t.peer[0] = reinterpret_cast<unsigned long long>(op.recv[pairpull ? peer : r]);
+      t.peer[1] = reinterpret_cast<unsigned long long>(op.recv[pairpull ? r : peer]);
       t.peer[2] = reinterpret_cast<unsigned long long>(op.out[r]);
       t.peer[3] = reinterpret_cast<unsigned long long>(op.out[peer]);
       t.peer[4] = reinterpret_cast<unsigned long long>(op.ctrl[r] + done);

@@ -81,8 +81,57 @@ def test_bf16_integer_bit_exact(op, M, N, K):
     assert bad.size == 0, f"{len(bad)} mismatches, first at {bad[:3].tolist()}"
 
 
+# Launches whose tiles leave the last wave of CTA pairs partly idle take the
+# stream-K tail (gemm_tc.cu SkParams): on a 148-SM B200, 4096 x 4096 is 128
+# tiles of 512x256 (1.73 waves of 74 pairs; 256 tiles of 256x256 with
+# AXONN_PAIR_MT=1), 4000 x 4100 x 1100 is 136 ragged tiles with a ragged K.
+SK_SHAPES = [(4096, 4096, 1024), (4000, 4100, 1100)]
+
+
+def _expect_stream_k():
+    import os
+    torch = require_cuda()
+    return (torch.cuda.get_device_properties(0).multi_processor_count == 148
+            and os.environ.get("AXONN_SK", "1") != "0"
+            and os.environ.get("AXONN_SCHED") != "static"
+            and os.environ.get("AXONN_GEMM_VARIANT") != "single")
+
+
 @pytest.mark.parametrize("op", list(OPS))
-@pytest.mark.parametrize("M,N,K", [(384, 768, 320), (300, 520, 200), (2048, 1536, 1024)])
+@pytest.mark.parametrize("M,N,K", SK_SHAPES)
+def test_stream_k_tail_integer_bit_exact(op, M, N, K):
+    """The contributor's fp32 partial sums (K-blocks [0, t0)) plus the
+    finisher's rest reach the exact integer sums: bit-exact after RNE."""
+    torch = require_cuda()
+    import paper_2502_08145_b200 as ax
+    A, B = _operands(op, M, N, K, "int")
+    want = synthdata.bf16_bits(synthdata.bf16_round(_oracle(op, A, B)))
+    n0 = ax.axonn_stream_k_launches()
+    got = bf16_bits_of(_run(op, A, B, M, N, torch.bfloat16))
+    if _expect_stream_k():
+        assert ax.axonn_stream_k_launches() == n0 + 1, "the stream-K tail did not run"
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, f"{len(bad)} mismatches, first at {bad[:3].tolist()}"
+
+
+@pytest.mark.parametrize("M,N,K", SK_SHAPES)
+def test_stream_k_tail_deterministic_and_fp32_output(M, N, K):
+    """Fixed split points and addition order: the same launch twice is
+    bit-identical on random inputs; the fp32-output dW product is exact on
+    integers."""
+    torch = require_cuda()
+    A, B = _operands("TN", M, N, K, "uniform")
+    c1 = bf16_bits_of(_run("TN", A, B, M, N, torch.bfloat16))
+    c2 = bf16_bits_of(_run("TN", A, B, M, N, torch.bfloat16))
+    assert np.array_equal(c1, c2)
+    A, B = _operands("TN", M, N, K, "int")
+    got = to_host_f64(_run("TN", A, B, M, N, torch.bfloat16, out_f32=True))
+    np.testing.assert_array_equal(got, _oracle("TN", A, B))
+
+
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("M,N,K", [(384, 768, 320), (300, 520, 200), (2048, 1536, 1024),
+                                   (4000, 4100, 1100)])
 def test_bf16_random_within_tolerance(op, M, N, K):
     torch = require_cuda()
     A, B = _operands(op, M, N, K, "uniform")
@@ -213,10 +262,12 @@ def test_full_size_sampled(op, M, N, K):
 
 @pytest.mark.parametrize("env", [{"AXONN_GEMM_VARIANT": "single"}, {"AXONN_PAIR_MT": "1"},
                                  {"AXONN_GROUP_M": "-8"}, {"AXONN_SCHED": "static"},
-                                 {"AXONN_SPLIT_RELEASE": "0"}])
+                                 {"AXONN_SPLIT_RELEASE": "0"}, {"AXONN_SK": "0"},
+                                 {"AXONN_MT2_DEEP": "0"}])
 def test_alternative_kernel_configurations(env):
     """The 1-CTA kernel, the 256x256 CTA-pair tile, the transposed raster,
-    static tile scheduling and whole-tile accumulator release (selected by
+    static tile scheduling, whole-tile accumulator release, no stream-K tail
+    and the 3-stage 512x256 pipeline (selected by
     environment, read once per process) pass the same bit-exact integer and
     full-size checks."""
     import os
@@ -225,6 +276,6 @@ def test_alternative_kernel_configurations(env):
     here = os.path.dirname(os.path.abspath(__file__))
     p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                         os.path.join(here, "test_gpu_gemm.py"), "-k",
-                        "integer or full_size or random"],
+                        "integer or full_size or random or stream_k"],
                        env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]

@@ -209,6 +209,10 @@ def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
     # both roles (the second arriver sums and writes both outputs)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM | ax.AXONN_LB_REVERSE)
+    # the pull variant: partials stay local, the second arriver reads the peer's
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM | ax.AXONN_LB_PAIRPULL)
+    check(ax, G, cfg, transposed, "int",
+          ax.AXONN_LB_PAIRSUM | ax.AXONN_LB_PAIRPULL | ax.AXONN_LB_REVERSE)
 
 
 @pytest.mark.parametrize("transposed", [False, True])

@@ -39,19 +39,47 @@ FIELDS = [(138, 139, 1024), (202, 204, 1)]
 def nvml_handle(local):
     import pynvml
     pynvml.nvmlInit()
+    global _SMI_BUS
     pr = torch.cuda.get_device_properties(local)
-    return pynvml.nvmlDeviceGetHandleByPciBusId(
-        f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+    _SMI_BUS = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+    return pynvml.nvmlDeviceGetHandleByPciBusId(_SMI_BUS)
 
 
 _FIELD = None
 
 
+_SMI_BUS = None
+_UNITS = {"B": 1, "KiB": 1024, "MiB": 1024 ** 2, "GiB": 1024 ** 3, "TiB": 1024 ** 4}
+
+
+def smi_counters():
+    """(tx, rx) data bytes summed over this GPU's links from
+    `nvidia-smi nvlink -gt d -i <bus id>` (the driver's per-link data
+    throughput counters), or None."""
+    import re
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", _SMI_BUS],
+                             capture_output=True, text=True, timeout=30).stdout
+    except Exception:
+        return None
+    tot = [0, 0]
+    hit = False
+    for key, i in (("Tx", 0), ("Rx", 1)):
+        for v, u in re.findall(rf"Data {key}:\s*([0-9]+)\s*([KMGT]?i?B)", out):
+            tot[i] += int(v) * _UNITS.get(u, 1)
+            hit = True
+    return tuple(tot) if hit else None
+
+
 def counters(h, nlinks=18):
     """(tx, rx) bytes summed over links (or the device total); None if no field
-    is available.  The first field set and scope that answers is kept."""
+    is available.  The first field set and scope that answers is kept; the
+    nvidia-smi per-link counters are the fallback."""
     import pynvml
     global _FIELD
+    if _FIELD == "smi":
+        return smi_counters()
     cands = [_FIELD] if _FIELD else [(f, sc) for f in FIELDS for sc in ("links", "all")]
     for (tx, rx, unit), scope in cands:
         scopes = range(nlinks) if scope == "links" else [0xFFFFFFFF]
@@ -68,7 +96,10 @@ def counters(h, nlinks=18):
         if ok:
             _FIELD = ((tx, rx, unit), scope)
             return tuple(tot)
-    return None
+    c = smi_counters()
+    if c is not None:
+        _FIELD = "smi"
+    return c
 
 
 def main():
@@ -146,7 +177,7 @@ def main():
                         "tx_GBps_over_call": tx / (ms * 1e-3) / 1e9,
                         "tx_over_eqs": tx / max(1, sum(eq.values()))})
         else:
-            rec["nvlink_counters"] = "unavailable (NVML field values 138/139)"
+            rec["nvlink_counters"] = "unavailable (NVML field values 138/139, nvidia-smi nvlink -gt d)"
         allr = [None] * world
         dist.all_gather_object(allr, rec)
         if rank == 0:
