@@ -84,6 +84,35 @@ def emit(obj) -> None:
     f.flush()
 
 
+def write_trace(path, c, ev, t_base, nrep, spec) -> None:
+    """Chrome-trace JSON (chrome://tracing, Perfetto) of the instrumented
+    per-layer steps: one complete event per layer phase and repetition on the
+    launching stream, CUDA-event timestamps relative to the first, one process
+    per rank (rank 0 gathers and writes)."""
+    import torch.distributed as dist
+    events = []
+    rank = dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
+    for key, lst in ev.items():
+        cat = "gemm_only" if key.endswith("_gemm") else ("sync" if key == "sync" else "alg1")
+        for r in range(nrep):
+            t0 = t_base.elapsed_time(lst[2 * r]) * 1e3
+            dur = lst[2 * r].elapsed_time(lst[2 * r + 1]) * 1e3
+            events.append({"name": key, "cat": cat, "ph": "X", "ts": round(t0, 3),
+                           "dur": round(dur, 3), "pid": rank, "tid": "compute stream",
+                           "args": {"rep": r}})
+    allr = [events]
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        allr = [None] * dist.get_world_size()
+        dist.all_gather_object(allr, events)
+    if rank == 0:
+        meta = [{"name": "process_name", "ph": "M", "pid": r, "args": {"name": f"rank {r}"}}
+                for r in range(len(allr))]
+        json.dump({"traceEvents": meta + [e for evs in allr for e in evs],
+                   "displayTimeUnit": "ms",
+                   "otherData": {"workload": spec.get("label", ""), "grid": spec.get("grid")}},
+                  open(path, "w"))
+
+
 def copy_raw(dst: int, src: int, nbytes: int, stream) -> None:
     """cudaMemcpyAsync between raw addresses (a library-owned buffer) on `stream`."""
     import ctypes
@@ -671,6 +700,8 @@ def run_config(c, spec, steps, warmup, e2e_on, exposure_on):
               for key in [f"{n_}_{ph}" for n_ in names for ph in ("fwd", "bwd", "fwd_gemm", "bwd_gemm")]
               + ["sync"]}
         acc_ms = {key: 0.0 for key in ev}
+        t_base = torch.cuda.Event(enable_timing=True)
+        t_base.record(stream)
         for rep in range(nrep):
             with torch.cuda.stream(stream):
                 for i, l in enumerate(L):
@@ -699,6 +730,8 @@ def run_config(c, spec, steps, warmup, e2e_on, exposure_on):
         for key, lst in ev.items():
             acc_ms[key] = max_over_ranks(sum(lst[2 * r].elapsed_time(lst[2 * r + 1])
                                              for r in range(nrep)) / nrep)
+        if getattr(args, "trace", None) and spec.get("primary", True):
+            write_trace(args.trace, c, ev, t_base, nrep, spec)
         per_layer = {}
         for n_ in names:
             for ph in ("fwd", "bwd"):
@@ -763,6 +796,8 @@ def main():
     ap.add_argument("--recompute", action="store_true",
                     help="activation checkpointing (PAPER.md:722-723): each layer's forward re-runs "
                          "before its backward; flops counted 8mkn as Narayanan et al.'s formula does")
+    ap.add_argument("--trace", default=None,
+                    help="write a Chrome-trace JSON of the per-layer phases (N > 1) to this path")
     ap.add_argument("--no-chain", action="store_true",
                     help="independent per-layer inputs (default: proj->fc1->fc2 chained)")
     args = ap.parse_args()
@@ -827,7 +862,7 @@ def main():
         plan.append(dict(label="data-parallel weak scaling (5B, 16384 tokens/GPU, model top-1)",
                          model="5B", m=16384 * world, grid=g, phase="A", grid_source=src))
         for sp in plan:
-            sp["blocks"], sp["chain"] = 1, not args.no_chain
+            sp["blocks"], sp["chain"], sp["primary"] = 1, not args.no_chain, False
             r = run_config(c, sp, args.sub_steps, max(3, args.warmup), False, True)
             subs.append({k: r[k] for k in ("label", "value", "per_gpu_tflops", "ms_per_step",
                                            "steps", "config", "overlap", "clocks",

@@ -274,9 +274,13 @@ enum {
   AXONN_LB_PAIRSUM = 32,     /* 2-rank bf16 axes: the sum finished in the epilogue */
   AXONN_LB_REVERSE = 64,     /* run each phase's ranks in reverse order (the
                                 pair-sum's second arriver is then rank 0)     */
-  AXONN_LB_PAIRPULL = 128    /* with AXONN_LB_PAIRSUM: each rank keeps its partial
+  AXONN_LB_PAIRPULL = 128,   /* with AXONN_LB_PAIRSUM: each rank keeps its partial
                                 in its own receive buffer and the second
                                 arriver reads the peer's over NVLink (pull)   */
+  AXONN_LB_NO_XSUM = 256     /* 2-rank bf16 axes: not the in-GEMM exchange sum
+                                (kXSum, the default at every K) but the
+                                exchange + local sum below the multimem.red
+                                threshold and multimem.red above it          */
 };
 enum {
   AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,
@@ -289,7 +293,9 @@ enum {
   AXONN_LB_PATH_FWD_EXCHANGE = 2048, AXONN_LB_PATH_BWD_EXCHANGE = 4096,
   AXONN_LB_PATH_DP_EXCHANGE = 8192,
   AXONN_LB_PATH_FWD_PAIRSUM = 16384, AXONN_LB_PATH_BWD_PAIRSUM = 32768,
-  AXONN_LB_PATH_DP_PAIRSUM = 65536
+  AXONN_LB_PATH_DP_PAIRSUM = 65536,
+  AXONN_LB_PATH_FWD_XSUM = 131072, AXONN_LB_PATH_BWD_XSUM = 262144,
+  AXONN_LB_PATH_DP_XSUM = 524288
 };
 axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
                                    const void* const* I_local, const void* const* W_hat,

@@ -396,10 +396,21 @@ void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_
   const int mode = axonn::fused_mode(S.g[axis], es, rows, cols, kdim,
                                      env_int("AXONN_RED_MIN_K", 8192),
                                      env_int("AXONN_EXCHANGE", 1) != 0,
-                                     env_int("AXONN_PAIRSUM", 0) != 0);
+                                     env_int("AXONN_PAIRSUM", 0) != 0,
+                                     env_int("AXONN_XSUM", 1));
   if (mode == axonn::kStore) return;
   f->elems = static_cast<size_t>(rows * cols);
   f->cols = cols;
+  if (mode == axonn::kXSum) {
+    // two receive sets of 2 slots (the call counter's parity picks one), the
+    // output, and the flag / done / counter block
+    f->epi.mode = mode;
+    reqs->push_back({axis, f->elems * es, &f->out});
+    reqs->push_back({axis, f->elems * es * 2, &f->recv});
+    reqs->push_back({axis, f->elems * es * 2, &f->recv2});
+    reqs->push_back({axis, axonn::xsum_ctrl_bytes(axonn::xsum_units(rows, cols)), &f->ctrl});
+    return;
+  }
   if (mode == axonn::kPairSum) {
     f->chunks = ((rows + 31) / 32) * ((cols + 63) / 64);
     f->epi.mode = mode;
@@ -427,6 +438,28 @@ bool fused_bind(axonn_fc::Fused* f, std::string* why) {
     return true;
   }
   const int P = S.g[f->axis], me = S.c[f->axis];
+  if (f->epi.mode == axonn::kXSum) {
+    unsigned long long recv[2], alt[2];
+    for (int q = 0; q < 2; ++q) {
+      recv[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv, q));
+      alt[q] = reinterpret_cast<unsigned long long>(axonn::sym_peer_ptr(&f->recv2, q));
+    }
+    void* pctrl = axonn::sym_peer_ptr(&f->ctrl, 1 - me);
+    if (!recv[0] || !recv[1] || !alt[0] || !alt[1] || !pctrl) {
+      *why = "peer address of an exchange-sum window unavailable";
+      return false;
+    }
+    const long long rows = static_cast<long long>(f->elems) / f->cols;
+    if (cudaMemset(f->ctrl.ptr, 0, axonn::xsum_ctrl_bytes(axonn::xsum_units(rows, f->cols))) !=
+            cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+      *why = "zeroing the exchange-sum control block failed";
+      return false;
+    }
+    f->epi = axonn::epi_xsum(me, rows, f->cols, recv, alt, f->out.ptr, f->ctrl.ptr, pctrl);
+    f->epi.mc = static_cast<unsigned long long>(env_int("AXONN_XSUM_OPT", 0));  // experiments
+    return true;
+  }
   if (f->epi.mode == axonn::kPairSum) {
     char* precv = static_cast<char*>(axonn::sym_peer_ptr(&f->recv, 1 - me));
     char* pout = static_cast<char*>(axonn::sym_peer_ptr(&f->out, 1 - me));
@@ -557,6 +590,15 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
 
 axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0,
                           void* act_z = nullptr) {
+  if (f.epi.mode == axonn::kXSum) {
+    // the GEMM summed what had landed; the sweep sums the rest as the peer's
+    // flags come up (no barrier) and advances the call counter
+    const long long rows = static_cast<long long>(f.elems) / f.cols;
+    CUDA_TRY(axonn::sym_xsum_sweep(f.recv.ptr, f.recv2.ptr, f.out.ptr, f.ctrl.ptr, rows, f.cols,
+                                   S.num_sms, st));
+    g_launches.fetch_add(1);
+    return AXONN_OK;
+  }
   if (f.epi.mode == axonn::kPairSum) {
     // the epilogues of both ranks finished the sums; wait for the peer's
     // share of the chunks (no barrier, no pass over the output)

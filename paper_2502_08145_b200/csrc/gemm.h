@@ -30,6 +30,18 @@ namespace axonn {
 //              outputs (peer[2] own, peer[3] peer's), then counts the chunk
 //              done on both ranks (peer[4] own counter, peer[5] peer's).
 //              slice = chunks per row of 64 columns.  bf16, ldc == N.
+//   kXSum      2-rank all-reduce by exchange, summed inside the GEMM: each
+//              16-B vector goes to slot `me` of both ranks' receive buffers
+//              (peer[q]: rank q's, slots of `slice` = M*N elements; peer_alt
+//              when *par is odd), as kExchange.  Per finished 32x128 output
+//              unit u (row/32 * ceil(N/128) + col/128) the warp raises the
+//              peer's flag (peer[4] + 4u) = epoch (*par + 1) after a system
+//              fence; a little later (never waiting) it sums units whose own
+//              flag (peer[3] + 4u, raised by the peer) shows the epoch: slot
+//              0 + slot 1 in fp32, one RNE rounding, to the output peer[2],
+//              and marks them done (peer[5] + 4u).  What is still open when
+//              the kernel ends is summed by sym_xsum_sweep, which also
+//              advances *par.  No barrier, no pass over the whole output.
 //   kRedLocal  red.global.add of each 16-B bf16 vector at mc + offset: the
 //              single-GPU loopback's stand-in for kMcRed when the device
 //              has no multicast support (axonn_loopback_step).
@@ -42,7 +54,8 @@ struct EpiTarget {
   unsigned long long peer_alt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int* par = nullptr;
 };
-enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4, kPairSum = 5 };
+enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4, kPairSum = 5,
+               kXSum = 6 };
 
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 

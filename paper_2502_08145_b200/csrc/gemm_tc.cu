@@ -328,6 +328,14 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int ld_acquire_sys_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_i(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ float4 ld_cg_f4(const float4* p) {  // L2 only: written by another SM
   float4 v;
   asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -484,6 +492,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the next kernel may be scheduled now (its
+  // CTAs take SMs as ours exit and run their prologue); this one touches no
+  // global memory before the previous kernel in the stream has completed.
+  // Both are no-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
@@ -635,10 +649,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
     uint8_t* stage_base = sEpi + ew * (Cfg::EPI_BOXES * 32 * 64 * 2);
     // kExchange double buffering: the receive buffers of this call (parity
     // counter written in stream order by the previous call's barrier kernel)
-    const unsigned long long* xbase =
-        (epi.mode == kExchange && epi.par && (*reinterpret_cast<const volatile int*>(epi.par) & 1))
-            ? epi.peer_alt
-            : epi.peer;
+    const bool xsum = epi.mode == kXSum;
+    const int xcalls = (epi.mode == kExchange || xsum) && epi.par
+                           ? *reinterpret_cast<const volatile int*>(epi.par) : 0;
+    const unsigned long long* xbase = (xcalls & 1) ? epi.peer_alt : epi.peer;
+    // kXSum: this call's flag value, the output units per row of 32, and the
+    // ring of this warp's units whose sum is still open (oldest first)
+    const int xepoch = xcalls + 1;
+    const int xupr = (N + 127) / 128;
+    constexpr int XQ = 4;
+    int xq[XQ];
+    int xn = 0;
+    // sum output unit u (32 rows x 128 columns): slot 0 + slot 1 of our
+    // receive buffer (own partial, the peer's over NVLink) -> RNE -> output
+    auto xsum_unit = [&](int uu) {
+      const int r0 = (uu / xupr) * 32, c0 = (uu % xupr) * 128;
+      const char* s0 = reinterpret_cast<const char*>(xbase[epi.me]);
+      const char* s1 = s0 + static_cast<uint64_t>(epi.slice) * 2;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int v = lane + 32 * i;
+        const int row = r0 + (v >> 4), col = c0 + (v & 15) * 8;
+        if (row < M && col < N) {
+          const uint64_t off = (static_cast<uint64_t>(row) * N + col) * 2;
+          uint4 a, b;
+          asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(s0 + off) : "memory");
+          asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(s1 + off) : "memory");
+          *reinterpret_cast<uint4*>(epi.peer[2] + off) = ptx::add_bf16x8(a, b);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) reinterpret_cast<int*>(epi.peer[5])[uu] = xepoch;
+    };
+    // sum the ring's units whose peer partial has landed, oldest first; with
+    // `patience` > 0 poll that many times for the oldest before leaving it
+    // (and the rest) to the sweep kernel
+    auto xsum_drain = [&](int patience) {
+      while (xn > 0) {
+        const int uu = xq[0];
+        const int f = ld_acquire_sys_i(reinterpret_cast<const int*>(epi.peer[3]) + uu);
+        if (!__all_sync(0xffffffffu, f == xepoch)) {
+          if (patience-- <= 0) return;
+          __nanosleep(200);
+          continue;
+        }
+        xsum_unit(uu);
+#pragma unroll
+        for (int q = 0; q + 1 < XQ; ++q) xq[q] = xq[q + 1];
+        --xn;
+      }
+    };
     int nstore = 0;  // TMA stores issued by this warp (alternate staging boxes)
     for (int seq = 0;; ++seq) {
       const int t = consume_tile(seq, false);
@@ -855,7 +917,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
                 // fused 2-rank all-reduce (host guarantees N % 8 == 0, ldc % 8 == 0)
                 ptx::multimem_red_add_bf16x8(
                     epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
-              } else if (epi.mode == kExchange) {
+              } else if (epi.mode == kExchange || epi.mode == kXSum) {
                 // all-reduce by exchange: this 16-B vector to slot `me` of every rank
                 const long long f = static_cast<long long>(grow) * N + gcol;
                 const uint64_t off =
@@ -901,6 +963,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
           if (lane == 0) ptx::mbar_arrive_leader(&tempty[mt]);
         }
       }
+      if (xsum && role != kRoleHead) {
+        // kXSum: this tile's partial (both copies) is performed system-wide
+        // before the peer's flags for its units go up
+        // (epi.mc bit 1, timing experiments only: no fence)
+        if (!(epi.mc & 2)) ptx::fence_sys();
+        __syncwarp();
+#pragma unroll 1
+        for (int mt = 0; mt < MT; ++mt) {
+          const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
+          const int col0 = tc.n0 + chalf * 128;
+          if (row0 >= M || col0 >= N) continue;
+          const int uu = (row0 / 32) * xupr + col0 / 128;
+          if (lane == 0) st_relaxed_sys_i(reinterpret_cast<int*>(epi.peer[4]) + uu, xepoch);
+          if (xn == XQ) {  // ring full: the oldest is left to the sweep
+#pragma unroll
+            for (int q = 0; q + 1 < XQ; ++q) xq[q] = xq[q + 1];
+            --xn;
+          }
+#pragma unroll
+          for (int q = 0; q < XQ; ++q)
+            if (q == xn) xq[q] = uu;
+          ++xn;
+        }
+        if (!(epi.mc & 1)) xsum_drain(0);  // epi.mc bit 0: every sum to the sweep
+      }
       if (role == kRoleHead) {
         // every lane's partial sums are written before the flag is raised
         __threadfence();
@@ -920,6 +1007,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
         acc_phase ^= 1;
       }
     }
+    if (xsum && !(epi.mc & 1)) xsum_drain(64);  // a short wait for the last units, the rest to the sweep
     if (epi.mode != kStore) ptx::fence_sys();  // remote writes performed before the kernel retires
     if (use_tma_store && lane == 0) ptx::tma_store_wait_all();
   }
@@ -928,6 +1016,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
   ptx::cluster_sync();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+  // the last CTA out returns the tile counter (and the exit count) to 0 for
+  // the slot's next launch: no memset between launches
+  if (dynamic && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(reinterpret_cast<unsigned*>(tile_counter + 1), 1u) == gridDim.x - 1) {
+      tile_counter[0] = 0;
+      tile_counter[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -990,11 +1088,13 @@ cudaError_t launch_single(const CUtensorMap& ma, const CUtensorMap& mb, void* C,
 
 int env_int(const char* name, int dflt);
 
-// Dynamic tile scheduling: a ring of global counters, one zeroed (in stream
-// order) per launch.  A slot is reused only after kSlots further launches, so
-// launches on different streams never share a live counter unless more than
-// kSlots GEMMs are in flight at once.  AXONN_SCHED=static disables it.
-// Called under the library mutex.
+// Dynamic tile scheduling: a ring of global counter pairs (tile counter, CTAs
+// finished), zeroed once; the last CTA of every launch resets its pair, so
+// consecutive GEMMs have no memset between them (which would also break the
+// programmatic dependent launch).  A slot is reused only after kSlots further
+// launches, so launches on different streams never share a live counter
+// unless more than kSlots GEMMs are in flight at once.  AXONN_SCHED=static
+// disables it.  Called under the library mutex.
 int* next_tile_counter(cudaStream_t stream) {
   static const bool dyn = [] {
     const char* v = std::getenv("AXONN_SCHED");
@@ -1004,10 +1104,20 @@ int* next_tile_counter(cudaStream_t stream) {
   constexpr int kSlots = 16384;
   static int* ring = nullptr;
   static int next = 0;
-  if (!ring && cudaMalloc(&ring, kSlots * sizeof(int)) != cudaSuccess) return nullptr;
-  int* c = ring + next;
+  if (!ring) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return nullptr;  // first use inside a capture: static scheduling for this launch
+    if (cudaMalloc(&ring, 2 * kSlots * sizeof(int)) != cudaSuccess) {
+      ring = nullptr;
+      return nullptr;
+    }
+    if (cudaMemset(ring, 0, 2 * kSlots * sizeof(int)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      return nullptr;
+  }
+  int* c = ring + 2 * next;
   next = (next + 1) % kSlots;
-  if (cudaMemsetAsync(c, 0, sizeof(int), stream) != cudaSuccess) return nullptr;
   return c;
 }
 
@@ -1090,9 +1200,20 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   static const int split = env_int("AXONN_SPLIT_RELEASE", 1) != 0;
   const SkParams sk = counter ? stream_k_plan(tiles, grid / 2, (K + BK - 1) / BK, MT, stream)
                               : SkParams();
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
-                                                       split, group_m, epi, counter, sk);
-  return cudaGetLastError();
+  // programmatic dependent launch (AXONN_PDL=0: plain stream order)
+  static const bool pdl = env_int("AXONN_PDL", 1) != 0;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(Cfg::THREADS);
+  lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kern, ma, mb, mc, use_tma_store, C, ldc, M, N, K, split, group_m,
+                            epi, counter, sk);
 }
 
 // MT = 2 takes the deep-pipeline configuration (4 operand stages, one
@@ -1178,6 +1299,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode == kScatter && (ldc != N || epi.slice % unit || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;
   if (epi.mode == kExchange && (ldc != N || epi.slice != M * N || epi.P < 1 || epi.P > 8))
+    return GemmStatus::kBadAlignment;
+  if (epi.mode == kXSum && (out_f32 || ldc != N || epi.slice != M * N || epi.P != 2 || !epi.par))
     return GemmStatus::kBadAlignment;
   if (epi.mode == kPairSum && (out_f32 || ldc != N || epi.slice != (N + 63) / 64))
     return GemmStatus::kBadAlignment;

@@ -226,6 +226,7 @@ struct LbOp {
   int axis = 0, P = 1, es = 2, mode = kStore;
   int64_t elems = 0;
   std::vector<char*> recv, out;  // per rank (scatter mode)
+  std::vector<char*> recv2;      // per rank (exchange-sum mode): the second receive set
   std::vector<char*> ctrl;       // per rank (pair-sum mode): tickets, done, calls
   int64_t cols = 0;
   long long chunks = 0;
@@ -277,6 +278,10 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   bool pairpull = false;
   if (const char* v = std::getenv("AXONN_PAIRSUM")) pairpull = std::atoi(v) == 2;
   if (flags & AXONN_LB_PAIRPULL) pairpull = true;
+  // the in-GEMM exchange sum (kXSum), as on the multi-GPU path (AXONN_XSUM)
+  int xsum2 = 1;
+  if (const char* v = std::getenv("AXONN_XSUM")) xsum2 = std::atoi(v);
+  if (flags & AXONN_LB_NO_XSUM) xsum2 = 0;
   const bool reverse = (flags & AXONN_LB_REVERSE) != 0;
   auto members = [&](int r, int axis) {
     std::vector<int> m(g[axis]);
@@ -295,7 +300,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     op->es = es;
     op->elems = rows * cols;
     if (op->P == 1) return AXONN_OK;
-    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2, pairsum2);
+    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2, pairsum2, xsum2);
     op->cols = cols;
     op->chunks = ((rows + 31) / 32) * ((cols + 63) / 64);
     if (op->mode == kStore) {
@@ -362,6 +367,23 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
           return rt_fail(AXONN_ERR_CUDA, "loopback: memset failed");
       }
     }
+    if (op->mode == kXSum) {  // two receive sets of 2 slots, output, control block
+      const long long U = xsum_units(op->elems / op->cols, op->cols);
+      op->recv.resize(G);
+      op->recv2.resize(G);
+      op->out.resize(G);
+      op->ctrl.resize(G);
+      for (int r = 0; r < G; ++r) {
+        op->recv[r] = static_cast<char*>(pool.get(op->elems * op->es * 2));
+        op->recv2[r] = static_cast<char*>(pool.get(op->elems * op->es * 2));
+        op->out[r] = static_cast<char*>(pool.get(op->elems * op->es));
+        op->ctrl[r] = static_cast<char*>(pool.get(xsum_ctrl_bytes(U)));
+        if (!op->recv[r] || !op->recv2[r] || !op->out[r] || !op->ctrl[r])
+          return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
+        if (cudaMemsetAsync(op->ctrl[r], 0, xsum_ctrl_bytes(U), st) != cudaSuccess)
+          return rt_fail(AXONN_ERR_CUDA, "loopback: memset failed");
+      }
+    }
     if (op->mode == kScatter || op->mode == kExchange) {
       // scatter: P slots of elems / P; exchange: P slots of elems (whole partials)
       const int64_t rbytes = op->elems * op->es * (op->mode == kExchange ? op->P : 1);
@@ -418,6 +440,17 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       t.peer[5] = reinterpret_cast<unsigned long long>(op.ctrl[peer] + done);
       return t;
     }
+    if (op.mode == kXSum) {  // as fused_bind in axonn.cpp
+      const std::vector<int> mem = members(r, op.axis);
+      const int me = cc[r][op.axis];
+      unsigned long long recv[2], alt[2];
+      for (int q = 0; q < 2; ++q) {
+        recv[q] = reinterpret_cast<unsigned long long>(op.recv[mem[q]]);
+        alt[q] = reinterpret_cast<unsigned long long>(op.recv2[mem[q]]);
+      }
+      return epi_xsum(me, op.elems / op.cols, op.cols, recv, alt, op.out[r], op.ctrl[r],
+                      op.ctrl[mem[1 - me]]);
+    }
     if (op.mode == kScatter || op.mode == kExchange) {
       const std::vector<int> mem = members(r, op.axis);
       unsigned long long peer[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -465,6 +498,15 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       }
       return AXONN_OK;
     }
+    if (op.mode == kXSum) {  // what the GEMMs left open (here: all of the first ranks')
+      for (int r = 0; r < G; ++r) {
+        if (sym_xsum_sweep(op.recv[r], op.recv2[r], op.out[r], op.ctrl[r], op.elems / op.cols,
+                           op.cols, rt_num_sms(), st) != cudaSuccess)
+          return rt_fail(AXONN_ERR_CUDA, "loopback: exchange-sum sweep launch failed");
+        rt_count_launch();
+      }
+      return AXONN_OK;
+    }
     if (op.mode == kExchange) {  // every rank sums its own P slots locally
       for (int r = 0; r < G; ++r) {
         OwnerOut o;
@@ -494,7 +536,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   // the reduced result of rank r -> its caller buffer
   auto deliver = [&](const LbOp& op, int r, void* dst) -> axonn_status_t {
     const char* src =
-        ((op.mode == kScatter || op.mode == kExchange || op.mode == kPairSum) && op.P == 2)
+        ((op.mode == kScatter || op.mode == kExchange || op.mode == kPairSum || op.mode == kXSum) &&
+         op.P == 2)
             ? op.out[r]
             : uc_of(op, r);
     if (op.elems &&
@@ -556,6 +599,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   if (fo.mode != kStore) {
     p |= fo.mode == kMcRed ? AXONN_LB_PATH_FWD_RED
          : fo.mode == kPairSum ? AXONN_LB_PATH_FWD_PAIRSUM
+         : fo.mode == kXSum ? AXONN_LB_PATH_FWD_XSUM
          : fo.mode == kExchange ? AXONN_LB_PATH_FWD_EXCHANGE : AXONN_LB_PATH_FWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fo, r, O[r])) != AXONN_OK) return s;
@@ -592,6 +636,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   if (fi.mode != kStore) {
     p |= fi.mode == kMcRed ? AXONN_LB_PATH_BWD_RED
          : fi.mode == kPairSum ? AXONN_LB_PATH_BWD_PAIRSUM
+         : fi.mode == kXSum ? AXONN_LB_PATH_BWD_XSUM
          : fi.mode == kExchange ? AXONN_LB_PATH_BWD_EXCHANGE : AXONN_LB_PATH_BWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fi, r, dI[r])) != AXONN_OK) return s;
@@ -642,6 +687,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     if ((s = owner_phase(fw)) != AXONN_OK) return s;
     p |= fw.mode == kMcRed ? AXONN_LB_PATH_DP_RED
          : fw.mode == kPairSum ? AXONN_LB_PATH_DP_PAIRSUM
+         : fw.mode == kXSum ? AXONN_LB_PATH_DP_XSUM
          : fw.mode == kExchange ? AXONN_LB_PATH_DP_EXCHANGE : AXONN_LB_PATH_DP_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fw, r, dW[r])) != AXONN_OK) return s;

@@ -170,6 +170,66 @@ __global__ void k_pair_wait(const uint32_t* done, uint32_t* calls, uint32_t tota
   *calls = c + 1u;
 }
 
+// kXSum sweep (see sym.h): one warp per 32x128 output unit, grid-stride.
+__global__ void k_xsum_sweep(const char* __restrict__ recv0, const char* __restrict__ recv1,
+                             char* __restrict__ out, int* ctrl, int M, int N, long long U,
+                             int* calls, unsigned* fin) {
+  const int c = *reinterpret_cast<volatile int*>(calls);
+  const int epoch = c + 1;
+  const char* s0 = (c & 1) ? recv1 : recv0;
+  const char* s1 = s0 + static_cast<uint64_t>(M) * N * 2;
+  const int* peerflag = ctrl;
+  const int* done = ctrl + U;
+  const int lane = threadIdx.x & 31;
+  const int upr = (N + 127) / 128;
+  const long long nw = static_cast<long long>(gridDim.x) * (blockDim.x / 32);
+  for (long long u = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; u < U;
+       u += nw) {
+    if (*reinterpret_cast<const volatile int*>(done + u) == epoch) continue;
+    long long spins = 0;
+    for (;;) {
+      int f;
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(f) : "l"(peerflag + u) : "memory");
+      if (__all_sync(0xffffffffu, f == epoch)) break;
+      __nanosleep(256);
+      if (++spins > (1LL << 26)) __trap();  // the peer never delivered: fail loudly
+    }
+    const int r0 = static_cast<int>(u / upr) * 32, c0 = static_cast<int>(u % upr) * 128;
+    for (int i = 0; i < 16; ++i) {
+      const int v = lane + 32 * i;
+      const int row = r0 + (v >> 4), col = c0 + (v & 15) * 8;
+      if (row < M && col < N) {
+        const uint64_t off = (static_cast<uint64_t>(row) * N + col) * 2;
+        uint4 a, b;
+        asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(s0 + off) : "memory");
+        asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(s1 + off) : "memory");
+        const uint32_t x[4] = {a.x, a.y, a.z, a.w}, y[4] = {b.x, b.y, b.z, b.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // slot 0 + slot 1 in fp32, one RNE rounding (R19)
+          const float lo = __uint_as_float(x[q] << 16) + __uint_as_float(y[q] << 16);
+          const float hi = __uint_as_float(x[q] & 0xFFFF0000u) + __uint_as_float(y[q] & 0xFFFF0000u);
+          __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+          o[q] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(out + off) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+  // the last CTA out advances the call counter (every CTA has read it)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(fin, 1u) == gridDim.x - 1) {
+      *fin = 0;
+      *calls = epoch;
+      __threadfence();
+    }
+  }
+}
+
 __global__ void k_barrier(ncclDevComm dc, uint32_t index, int* ctr) {
   ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), index);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
@@ -355,7 +415,7 @@ cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* d
 }
 
 int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
-               bool exchange2, bool pairsum2) {
+               bool exchange2, bool pairsum2, int xsum2) {
   const int64_t n = rows * cols;
   const int unit = 16 / es;  // elements per 16-B epilogue unit
   // not fused: a 1-rank axis, an empty output, rows not a whole number of
@@ -363,6 +423,8 @@ int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_
   if (P < 2 || n <= 0 || cols % unit || kdim <= 0) return kStore;
   // 2-rank bf16: the sum finished inside the epilogue (no post pass, no barrier)
   if (es == 2 && P == 2 && pairsum2) return kPairSum;
+  // 2-rank bf16: exchange, summed inside the GEMM as partials land
+  if (es == 2 && P == 2 && (xsum2 == 1 || (xsum2 == 2 && kdim < red_min_k))) return kXSum;
   // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
   if (es == 2 && P == 2 && kdim >= red_min_k) return kMcRed;
   // 2-rank axes: exchange whole partials, then sum locally (no owner broadcast)
@@ -383,6 +445,26 @@ EpiTarget epi_exchange(int P, int me, long long n, const unsigned long long* rec
     t.peer_alt[q] = recv_alt ? recv_alt[q] : recv[q];
   }
   t.par = par;
+  return t;
+}
+
+EpiTarget epi_xsum(int me, long long rows, long long cols, const unsigned long long* recv,
+                   const unsigned long long* recv_alt, void* out, void* ctrl, void* peer_ctrl) {
+  EpiTarget t;
+  t.mode = kXSum;
+  t.P = 2;
+  t.me = me;
+  t.slice = rows * cols;
+  const long long U = xsum_units(rows, cols);
+  for (int q = 0; q < 2; ++q) {
+    t.peer[q] = recv[q];
+    t.peer_alt[q] = recv_alt[q];
+  }
+  t.peer[2] = reinterpret_cast<unsigned long long>(out);
+  t.peer[3] = reinterpret_cast<unsigned long long>(ctrl);
+  t.peer[4] = reinterpret_cast<unsigned long long>(peer_ctrl);
+  t.peer[5] = reinterpret_cast<unsigned long long>(static_cast<char*>(ctrl) + U * 4);
+  t.par = reinterpret_cast<const int*>(static_cast<char*>(ctrl) + xsum_calls_off(U));
   return t;
 }
 
@@ -420,6 +502,20 @@ cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* d
 cudaError_t sym_pair_wait(const void* done, void* calls, uint32_t total, cudaStream_t st) {
   k_pair_wait<<<1, 32, 0, st>>>(static_cast<const uint32_t*>(done), static_cast<uint32_t*>(calls),
                                 total);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_xsum_sweep(const void* recv0, const void* recv1, void* out, void* ctrl,
+                           long long rows, long long cols, int num_sms, cudaStream_t st) {
+  const long long U = xsum_units(rows, cols);
+  if (U <= 0) return cudaSuccess;
+  char* c = static_cast<char*>(ctrl);
+  long long blocks = (U + 7) / 8;
+  if (blocks > 2LL * num_sms) blocks = 2LL * num_sms;
+  k_xsum_sweep<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+      static_cast<const char*>(recv0), static_cast<const char*>(recv1), static_cast<char*>(out),
+      reinterpret_cast<int*>(c), static_cast<int>(rows), static_cast<int>(cols), U,
+      reinterpret_cast<int*>(c + xsum_calls_off(U)), reinterpret_cast<unsigned*>(c + xsum_fin_off(U)));
   return cudaGetLastError();
 }
 

@@ -96,8 +96,30 @@ cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0, int* ctr = n
 // es-byte elements.  kStore means "not fused" (NCCL, or no reduction when
 // P == 1).  2-rank bf16 axes use multimem.red when kdim >= red_min_k, else
 // (exchange2) the exchange of whole partials, else the scatter + owner phase.
+// xsum2: 1 = 2-rank bf16 axes sum inside the GEMM (kXSum) at every K;
+// 2 = only below red_min_k (multimem.red above); 0 = never.
 int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
-               bool exchange2, bool pairsum2);
+               bool exchange2, bool pairsum2, int xsum2 = 0);
+// kXSum: the control block (per rank, symmetric): [0, 4U) the flags the peer
+// raises per 32x128 output unit, [4U, 8U) this rank's done marks, then the
+// call counter (the parity of the receive set, the flag epoch) and the
+// sweep's finished-CTA counter.  Zeroed once at creation.
+inline long long xsum_units(long long rows, long long cols) {
+  return ((rows + 31) / 32) * ((cols + 127) / 128);
+}
+inline size_t xsum_ctrl_bytes(long long units) { return static_cast<size_t>(units) * 8 + 256; }
+inline size_t xsum_calls_off(long long units) { return static_cast<size_t>(units) * 8 + 128; }
+inline size_t xsum_fin_off(long long units) { return static_cast<size_t>(units) * 8 + 192; }
+// The sums the GEMM left open: every unit not marked done waits for the
+// peer's flag, then slot 0 + slot 1 of the receive set -> RNE -> out.  The
+// last CTA advances the call counter.  recv0 / recv1: this rank's receive
+// sets (2 slots of rows*cols bf16 each).
+cudaError_t sym_xsum_sweep(const void* recv0, const void* recv1, void* out, void* ctrl,
+                           long long rows, long long cols, int num_sms, cudaStream_t st);
+// kXSum epilogue target: recv[q] / recv_alt[q] rank q's receive sets, out this
+// rank's output, ctrl / peer_ctrl the control blocks (xsum_ctrl_bytes).
+EpiTarget epi_xsum(int me, long long rows, long long cols, const unsigned long long* recv,
+                   const unsigned long long* recv_alt, void* out, void* ctrl, void* peer_ctrl);
 // kPairSum: the control block of a pair-sum reduction (per rank, symmetric):
 // [0, 4*chunks) arbitration tickets (rank 0's copy is the shared one),
 // then the done counter and the call counter.

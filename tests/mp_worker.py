@@ -265,14 +265,16 @@ def main():
     shapes = [(256, 512, 1024), (384, 192, 320)]
     for cfg in ogrid.enumerate_configs(world):
         results = {}
-        # "red": 2-rank axes reduce with multimem.red; "exchange": 2-rank axes
+        # "xsum": 2-rank axes exchange partials and sum them inside the GEMM
+        # (the default); "red": 2-rank axes reduce with multimem.red; "exchange": 2-rank axes
         # exchange whole partials and sum locally; "scatter": 2-rank axes use
         # the scatter + owner phase; "0": NCCL collectives (AXONN_FUSED=0)
-        for fused in ("red", "exchange", "pairsum", "pairpull", "scatter", "0"):
+        for fused in ("xsum", "red", "exchange", "pairsum", "pairpull", "scatter", "0"):
             os.environ["AXONN_FUSED"] = "0" if fused == "0" else "1"
             os.environ["AXONN_RED_MIN_K"] = "0" if fused == "red" else str(1 << 30)
             os.environ["AXONN_EXCHANGE"] = "0" if fused == "scatter" else "1"
             os.environ["AXONN_PAIRSUM"] = {"pairsum": "1", "pairpull": "2"}.get(fused, "0")
+            os.environ["AXONN_XSUM"] = "1" if fused == "xsum" else "0"
             ax.axonn_grid_init(*cfg)
             if fused == "red" and rank == 0:
                 print(f"cfg={cfg} fused status:",
@@ -297,7 +299,7 @@ def main():
                             for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
                                 assert np.array_equal(a, b), f"zero-copy differs {cfg}"
             run_chain(cfg, "uniform", torch.bfloat16, rank)
-            if fused in ("red", "exchange", "pairsum", "pairpull", "0"):
+            if fused in ("xsum", "red", "exchange", "pairsum", "pairpull", "0"):
                 run_graph(cfg, rank)
                 run_empty(cfg, rank)
             if fused == "0":

@@ -263,11 +263,12 @@ def test_full_size_sampled(op, M, N, K):
 @pytest.mark.parametrize("env", [{"AXONN_GEMM_VARIANT": "single"}, {"AXONN_PAIR_MT": "1"},
                                  {"AXONN_GROUP_M": "-8"}, {"AXONN_SCHED": "static"},
                                  {"AXONN_SPLIT_RELEASE": "0"}, {"AXONN_SK": "0"},
-                                 {"AXONN_MT2_DEEP": "0"}])
+                                 {"AXONN_MT2_DEEP": "0"}, {"AXONN_PDL": "0"}])
 def test_alternative_kernel_configurations(env):
     """The 1-CTA kernel, the 256x256 CTA-pair tile, the transposed raster,
-    static tile scheduling, whole-tile accumulator release, no stream-K tail
-    and the 3-stage 512x256 pipeline (selected by
+    static tile scheduling, whole-tile accumulator release, no stream-K tail,
+    the 3-stage 512x256 pipeline and plain stream order instead of the
+    programmatic dependent launch (selected by
     environment, read once per process) pass the same bit-exact integer and
     full-size checks."""
     import os

@@ -138,10 +138,13 @@ def _expected_paths(cfg, transposed, flags, grad_f32=False):
     ax_f, ax_b = (0, 1) if transposed else (1, 0)
     want = set()
     red2, no_x, pair = bool(flags & 1), bool(flags & 16), bool(flags & 32)
+    xs = not (flags & 256)
 
     def two(name, es2=True):
         if pair and es2:
             return f"{name}_pairsum"
+        if xs and es2:
+            return f"{name}_xsum"
         return f"{name}_red" if (red2 and es2) else (f"{name}_scatter" if no_x else f"{name}_exchange")
     for name, P in (("fwd", cfg[ax_f]), ("bwd", cfg[ax_b])):
         if P == 2:
@@ -199,12 +202,17 @@ CASES = [(G, cfg) for G in (2, 3, 4, 6, 8) for cfg in grid.enumerate_configs(G)]
 @pytest.mark.parametrize("transposed", [False, True])
 @pytest.mark.parametrize("G,cfg", CASES, ids=[f"{c[0]}{c[1]}{c[2]}{c[3]}" for _, c in CASES])
 def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
-    # default 2-rank mode for these short K (exchange of whole partials) and
-    # the copy-engine AG_z; multimem.red forced on 2-rank axes with the
-    # SM-pull AG_z; the 2-rank scatter + owner phase (exchange off)
+    # default 2-rank mode (the exchange summed inside the GEMM, kXSum: here
+    # the first rank of each pair leaves its sums to the sweep, the second
+    # sums in the epilogue) and the copy-engine AG_z; the exchange + local
+    # sum; multimem.red forced on 2-rank axes with the SM-pull AG_z; the
+    # 2-rank scatter + owner phase (exchange off)
+    nx = ax.AXONN_LB_NO_XSUM
     check(ax, G, cfg, transposed, "int", 0)
-    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
-    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_REVERSE)
+    check(ax, G, cfg, transposed, "int", nx)
+    check(ax, G, cfg, transposed, "int", nx | ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
+    check(ax, G, cfg, transposed, "int", nx | ax.AXONN_LB_NO_EXCHANGE)
     # the sum finished inside the epilogue (kPairSum), each rank of a pair in
     # both roles (the second arriver sums and writes both outputs)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM)
@@ -219,7 +227,8 @@ def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
 @pytest.mark.parametrize("G,cfg", [(G, c) for G, c in CASES if G in (4, 6, 8)],
                          ids=[f"{c[0]}{c[1]}{c[2]}{c[3]}" for G, c in CASES if G in (4, 6, 8)])
 def test_every_grid_uniform_within_tolerance(ax, G, cfg, transposed):
-    check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_RED_ALWAYS)
+    check(ax, G, cfg, transposed, "uniform", 0)
+    check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 2, 1), (1, 1, 1, 2), (1, 1, 4, 2), (1, 1, 2, 4),
@@ -239,12 +248,14 @@ def test_emulated_multicast_agrees(ax, cfg):
     """Without a multicast object (red.global.add / plain stores) the results
     are the same bits (the stand-in is only used on devices without NVLS)."""
     G = int(np.prod(cfg))
-    check(ax, G, cfg, False, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_EMULATE_MC)
+    check(ax, G, cfg, False, "int",
+          ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_EMULATE_MC | ax.AXONN_LB_NO_XSUM)
 
 
 def test_multicast_object_used_when_available(ax):
     torch = require_cuda()
-    _, _, paths = run_loopback(ax, *SHAPES[2], (1, 2, 1, 1), False, "int", ax.AXONN_LB_RED_ALWAYS)
+    _, _, paths = run_loopback(ax, *SHAPES[2], (1, 2, 1, 1), False, "int",
+                               ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)
     print("loopback multicast object:", "multicast" in paths)
     assert "fwd_red" in paths   # normal layer: the forward all-reduce runs over Y
 
@@ -273,7 +284,7 @@ def test_long_k_tile_configuration(cfg):
         "import test_gpu_loopback as t, paper_2502_08145_b200 as ax\n"
         "for T in (False, True):\n"
         "    t.check(ax, %d, %r, T, 'int', 0)\n"
-        "    t.check(ax, %d, %r, T, 'int', ax.AXONN_LB_RED_ALWAYS)\n"
+        "    t.check(ax, %d, %r, T, 'int', ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)\n"
         "print('MT2_OK')\n" % (ROOT, os.path.join(ROOT, "tests"), int(np.prod(cfg)), cfg,
                                int(np.prod(cfg)), cfg))
     env = dict(os.environ, AXONN_PAIR_MT_FUSED="2")
@@ -289,8 +300,9 @@ FULL = [  # (name, h, m, grid, layers): tensor-parallel proxies of BASELINE C3/C
 ]
 
 
+@pytest.mark.parametrize("flags", [0, 256], ids=["xsum", "red_exchange"])
 @pytest.mark.parametrize("name,h,m,cfg,which", FULL, ids=[f[0] for f in FULL])
-def test_full_size_tensor_parallel(ax, name, h, m, cfg, which):
+def test_full_size_tensor_parallel(ax, name, h, m, cfg, which, flags):
     """Full-size GPT-block layers on tensor-parallel grids, every rank on this
     GPU through the fused collectives in the launch configuration the
     multi-GPU bench uses (K >= 8192 launches take 512x256 tiles and, on 2-rank
@@ -316,7 +328,7 @@ def test_full_size_tensor_parallel(ax, name, h, m, cfg, which):
             O.append(torch.empty((g.m_l, g.n_l), dtype=torch.bfloat16, device="cuda"))
             dI.append(torch.empty((g.m_l, g.k_l), dtype=torch.bfloat16, device="cuda"))
             dW.append(torch.empty((g.what_len,), dtype=torch.bfloat16, device="cuda"))
-        paths = ax.axonn_loopback_step(mm, k, n, cfg, I, Wh, dO, O, dI, dW, T)
+        paths = ax.axonn_loopback_step(mm, k, n, cfg, I, Wh, dO, O, dI, dW, T, flags=flags)
         ar = np.arange(1024)
 
         def sampled(A, B, rows, cols):
@@ -395,8 +407,9 @@ def test_gelu_layer(ax, cfg, transposed):
     elementwise pass after the other forward modes; dGeLU before line 11."""
     G = int(np.prod(cfg))
     paths = check_act(ax, G, cfg, transposed, 0)
-    check_act(ax, G, cfg, transposed, ax.AXONN_LB_RED_ALWAYS)
-    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE)
+    paths_x = check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_XSUM)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE | ax.AXONN_LB_NO_XSUM)
     ax_f = 0 if transposed else 1
     if cfg[ax_f] == 2:
-        assert "fwd_exchange" in paths
+        assert "fwd_xsum" in paths and "fwd_exchange" in paths_x

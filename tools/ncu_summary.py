@@ -25,7 +25,12 @@ SCALE = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "ns
          "hz": 1e-9, "Khz": 1e-6, "Mhz": 1e-3, "Ghz": 1.0}
 
 
-def main(rep, out_md, traffic_json=None):
+SHAPE_NAMES = [f"{l}_{p}" for l in ("qkv", "proj", "fc1", "fc2") for p in ("fwd", "dI", "dW")]
+
+
+def main(rep, out_md, traffic_json=None, pick=None):
+    """pick="odd": keep launches 1, 3, 5, ... (tools/gemm_shapes.py --reps 1
+    --rounds 1 runs each C2 shape twice: warm-up, then the measured launch)."""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -40,6 +45,10 @@ def main(rep, out_md, traffic_json=None):
                 v = float(r[i].replace(",", "")) if r[i] not in ("", "n/a") else float("nan")
                 d[key] = v * SCALE.get(units[i], 1.0)
         recs.append(d)
+    if pick == "odd":
+        recs = recs[1::2]
+        for d, name in zip(recs, SHAPE_NAMES):
+            d["kernel"] = name + " " + d["kernel"].split("::")[-1]
     lines = ["| # | kernel | grid | time ms | DRAM read GB | DRAM write GB | UTCHMMA % peak | hmma pipe % active | SM GHz |",
              "|---|---|---|---|---|---|---|---|---|"]
     for i, d in enumerate(recs):
@@ -63,4 +72,5 @@ def main(rep, out_md, traffic_json=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "-" else None,
+         sys.argv[4] if len(sys.argv) > 4 else None)
