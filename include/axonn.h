@@ -277,10 +277,9 @@ enum {
   AXONN_LB_PAIRPULL = 128,   /* with AXONN_LB_PAIRSUM: each rank keeps its partial
                                 in its own receive buffer and the second
                                 arriver reads the peer's over NVLink (pull)   */
-  AXONN_LB_NO_XSUM = 256     /* 2-rank bf16 axes: not the in-GEMM exchange sum
-                                (kXSum, the default at every K) but the
-                                exchange + local sum below the multimem.red
-                                threshold and multimem.red above it          */
+  AXONN_LB_XSUM = 256        /* 2-rank bf16 axes at every K: the exchange summed
+                                inside the GEMM (kXSum, AXONN_XSUM=1 on the
+                                multi-GPU path; opt-in, measured slower)      */
 };
 enum {
   AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,

@@ -397,7 +397,7 @@ void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_
                                      env_int("AXONN_RED_MIN_K", 8192),
                                      env_int("AXONN_EXCHANGE", 1) != 0,
                                      env_int("AXONN_PAIRSUM", 0) != 0,
-                                     env_int("AXONN_XSUM", 1));
+                                     env_int("AXONN_XSUM", 0));
   if (mode == axonn::kStore) return;
   f->elems = static_cast<size_t>(rows * cols);
   f->cols = cols;

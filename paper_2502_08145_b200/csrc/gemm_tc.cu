@@ -281,7 +281,8 @@ struct PairCfg {
   // per warp: 32 x 64 bf16 staging boxes; with two, the TMA store of one overlaps filling the other
   static constexpr int EPI_BOXES = DEEP ? 1 : 2;
   static constexpr int EPI_BYTES = EPI_WARPS * EPI_BOXES * 32 * 64 * 2;
-  static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+  // + the kXSum unit ring (256 entries) and its counters
+  static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256 + 1024 + 32;
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
@@ -398,6 +399,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
   uint64_t* tq_empty = tq_full + 4;   // consumer releases, counted on the leader
   int* tq = reinterpret_cast<int*>(tq_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
+  // kXSum: ring of finished output units (epilogue warps push, helper warps
+  // 2 and 3 sum them), 256 entries; then the per-helper heads, the tail and
+  // the count of epilogue warps that are done
+  int* xring = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full) + 256);
+  unsigned* xhead = reinterpret_cast<unsigned*>(xring + 256);  // [2]
+  unsigned* xtail = xhead + 2;
+  unsigned* xfin = xhead + 3;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -488,6 +496,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  if (warp == 3) {
+    for (int i = lane; i < 256; i += 32) xring[i] = 0;
+    if (lane < 4) xhead[lane] = 0;  // heads, tail, finished count
+  }
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -498,6 +510,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
   // Both are no-ops without the launch attribute.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  // kExchange / kXSum: the call counter picks the receive set (device-side
+  // double buffering); kXSum: the flag epoch of this call
+  const bool xsum = epi.mode == kXSum;
+  const int xcalls = (epi.mode == kExchange || xsum) && epi.par
+                         ? *reinterpret_cast<const volatile int*>(epi.par) : 0;
+  const unsigned long long* xbase = (xcalls & 1) ? epi.peer_alt : epi.peer;
+  const int xepoch = xcalls + 1;
+  const int xupr = (N + 127) / 128;
+  // kXSum: sum output unit u (32 rows x 128 columns) with the whole warp:
+  // slot 0 + slot 1 of our receive set (own partial; the peer's, landed over
+  // NVLink) in fp32, one RNE rounding, to the output; mark it done
+  auto xsum_unit = [&](int uu) {
+    const int r0 = (uu / xupr) * 32, c0 = (uu % xupr) * 128;
+    const char* s0 = reinterpret_cast<const char*>(xbase[epi.me]);
+    const char* s1 = s0 + static_cast<uint64_t>(epi.slice) * 2;
+#pragma unroll 8
+    for (int i = 0; i < 16; ++i) {
+      const int v = lane + 32 * i;
+      const int row = r0 + (v >> 4), col = c0 + (v & 15) * 8;
+      if (row < M && col < N) {
+        const uint64_t off = (static_cast<uint64_t>(row) * N + col) * 2;
+        uint4 a, b;
+        asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(s0 + off) : "memory");
+        asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(s1 + off) : "memory");
+        *reinterpret_cast<uint4*>(epi.peer[2] + off) = ptx::add_bf16x8(a, b);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) reinterpret_cast<int*>(epi.peer[5])[uu] = xepoch;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
@@ -628,6 +673,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
       }
     }
     __syncwarp();
+  } else if (warp == 2 || warp == 3) {
+    // ------------------------------------------------ kXSum helpers (both CTAs)
+    // Helper c sums ring slots c, c + 2, ... in order once the peer's flag for
+    // the unit is up.  It never holds the epilogue back for long: when the
+    // ring backs up (the peer lags) or the epilogue is done and the wait
+    // budget is spent, the unit is left to the sweep kernel.
+    if (xsum) {
+      const int c = warp - 2;
+      int end_budget = 400;  // polls of ~0.2 us once every epilogue warp is done
+      for (unsigned k = 0;; ++k) {
+        const unsigned sl = 2 * k + c;
+        int entry = 0;
+        bool stop = false;
+        for (;;) {
+          entry = *reinterpret_cast<volatile int*>(&xring[sl & 255]);
+          if ((entry & 255) == static_cast<int>((sl >> 8) % 255 + 1)) break;
+          if (*reinterpret_cast<volatile unsigned*>(xfin) == Cfg::EPI_WARPS &&
+              *reinterpret_cast<volatile unsigned*>(xtail) <= sl) {
+            stop = true;
+            break;
+          }
+          __nanosleep(64);
+        }
+        if (stop) break;
+        __threadfence_block();  // the pushing warp's fence precedes its ring store
+        const int uu = entry >> 8;
+        bool ok = false;
+        for (;;) {
+          const int f = ld_acquire_sys_i(reinterpret_cast<const int*>(epi.peer[3]) + uu);
+          ok = __all_sync(0xffffffffu, f == xepoch);
+          if (ok) break;
+          const unsigned tail = *reinterpret_cast<volatile unsigned*>(xtail);
+          const bool done = *reinterpret_cast<volatile unsigned*>(xfin) == Cfg::EPI_WARPS;
+          if (tail - sl > 192 || (done && --end_budget < 0)) break;
+          __nanosleep(200);
+        }
+        if (ok) xsum_unit(uu);
+        __syncwarp();
+        if (lane == 0) *reinterpret_cast<volatile unsigned*>(&xhead[c]) = k + 1;
+      }
+    }
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (both CTAs)
     // TMEM -> registers (thread = row) -> bf16 -> XOR-swizzled smem -> 16-B
@@ -649,58 +736,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
     uint8_t* stage_base = sEpi + ew * (Cfg::EPI_BOXES * 32 * 64 * 2);
     // kExchange double buffering: the receive buffers of this call (parity
     // counter written in stream order by the previous call's barrier kernel)
-    const bool xsum = epi.mode == kXSum;
-    const int xcalls = (epi.mode == kExchange || xsum) && epi.par
-                           ? *reinterpret_cast<const volatile int*>(epi.par) : 0;
-    const unsigned long long* xbase = (xcalls & 1) ? epi.peer_alt : epi.peer;
-    // kXSum: this call's flag value, the output units per row of 32, and the
-    // ring of this warp's units whose sum is still open (oldest first)
-    const int xepoch = xcalls + 1;
-    const int xupr = (N + 127) / 128;
-    constexpr int XQ = 4;
-    int xq[XQ];
-    int xn = 0;
-    // sum output unit u (32 rows x 128 columns): slot 0 + slot 1 of our
-    // receive buffer (own partial, the peer's over NVLink) -> RNE -> output
-    auto xsum_unit = [&](int uu) {
-      const int r0 = (uu / xupr) * 32, c0 = (uu % xupr) * 128;
-      const char* s0 = reinterpret_cast<const char*>(xbase[epi.me]);
-      const char* s1 = s0 + static_cast<uint64_t>(epi.slice) * 2;
-#pragma unroll 4
-      for (int i = 0; i < 16; ++i) {
-        const int v = lane + 32 * i;
-        const int row = r0 + (v >> 4), col = c0 + (v & 15) * 8;
-        if (row < M && col < N) {
-          const uint64_t off = (static_cast<uint64_t>(row) * N + col) * 2;
-          uint4 a, b;
-          asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(s0 + off) : "memory");
-          asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(s1 + off) : "memory");
-          *reinterpret_cast<uint4*>(epi.peer[2] + off) = ptx::add_bf16x8(a, b);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) reinterpret_cast<int*>(epi.peer[5])[uu] = xepoch;
-    };
-    // sum the ring's units whose peer partial has landed, oldest first; with
-    // `patience` > 0 poll that many times for the oldest before leaving it
-    // (and the rest) to the sweep kernel
-    auto xsum_drain = [&](int patience) {
-      while (xn > 0) {
-        const int uu = xq[0];
-        const int f = ld_acquire_sys_i(reinterpret_cast<const int*>(epi.peer[3]) + uu);
-        if (!__all_sync(0xffffffffu, f == xepoch)) {
-          if (patience-- <= 0) return;
-          __nanosleep(200);
-          continue;
-        }
-        xsum_unit(uu);
-#pragma unroll
-        for (int q = 0; q + 1 < XQ; ++q) xq[q] = xq[q + 1];
-        --xn;
-      }
-    };
     int nstore = 0;  // TMA stores issued by this warp (alternate staging boxes)
     for (int seq = 0;; ++seq) {
       const int t = consume_tile(seq, false);
@@ -965,28 +1000,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
       }
       if (xsum && role != kRoleHead) {
         // kXSum: this tile's partial (both copies) is performed system-wide
-        // before the peer's flags for its units go up
-        // (epi.mc bit 1, timing experiments only: no fence)
+        // before the peer's flags for its units go up; the units then go to
+        // the helper warps (epi.mc bit 0, experiments: all to the sweep;
+        // bit 1: no fence, timing only)
         if (!(epi.mc & 2)) ptx::fence_sys();
         __syncwarp();
+        if (lane == 0) {
 #pragma unroll 1
-        for (int mt = 0; mt < MT; ++mt) {
-          const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
-          const int col0 = tc.n0 + chalf * 128;
-          if (row0 >= M || col0 >= N) continue;
-          const int uu = (row0 / 32) * xupr + col0 / 128;
-          if (lane == 0) st_relaxed_sys_i(reinterpret_cast<int*>(epi.peer[4]) + uu, xepoch);
-          if (xn == XQ) {  // ring full: the oldest is left to the sweep
-#pragma unroll
-            for (int q = 0; q + 1 < XQ; ++q) xq[q] = xq[q + 1];
-            --xn;
+          for (int mt = 0; mt < MT; ++mt) {
+            const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
+            const int col0 = tc.n0 + chalf * 128;
+            if (row0 >= M || col0 >= N) continue;
+            const int uu = (row0 / 32) * xupr + col0 / 128;
+            st_relaxed_sys_i(reinterpret_cast<int*>(epi.peer[4]) + uu, xepoch);
+            if (epi.mc & 1) continue;
+            // slot s of the ring: helper s & 1 consumes it; wait until that
+            // helper is done with slot s - 256 (helpers never wait long)
+            const unsigned sl = atomicAdd(xtail, 1u);
+            while (static_cast<int>((sl >> 1) - *reinterpret_cast<volatile unsigned*>(&xhead[sl & 1])) >= 128)
+              __nanosleep(64);
+            *reinterpret_cast<volatile int*>(&xring[sl & 255]) =
+                uu * 256 + static_cast<int>((sl >> 8) % 255 + 1);  // round stamp 1..255
           }
-#pragma unroll
-          for (int q = 0; q < XQ; ++q)
-            if (q == xn) xq[q] = uu;
-          ++xn;
         }
-        if (!(epi.mc & 1)) xsum_drain(0);  // epi.mc bit 0: every sum to the sweep
+        __syncwarp();
       }
       if (role == kRoleHead) {
         // every lane's partial sums are written before the flag is raised
@@ -1007,7 +1044,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
         acc_phase ^= 1;
       }
     }
-    if (xsum && !(epi.mc & 1)) xsum_drain(64);  // a short wait for the last units, the rest to the sweep
+    if (xsum && lane == 0) atomicAdd(xfin, 1u);  // this warp pushes no more units
     if (epi.mode != kStore) ptx::fence_sys();  // remote writes performed before the kernel retires
     if (use_tma_store && lane == 0) ptx::tma_store_wait_all();
   }

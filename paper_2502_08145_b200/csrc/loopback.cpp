@@ -278,10 +278,10 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   bool pairpull = false;
   if (const char* v = std::getenv("AXONN_PAIRSUM")) pairpull = std::atoi(v) == 2;
   if (flags & AXONN_LB_PAIRPULL) pairpull = true;
-  // the in-GEMM exchange sum (kXSum), as on the multi-GPU path (AXONN_XSUM)
-  int xsum2 = 1;
+  // the in-GEMM exchange sum (kXSum, opt-in), as on the multi-GPU path (AXONN_XSUM)
+  int xsum2 = 0;
   if (const char* v = std::getenv("AXONN_XSUM")) xsum2 = std::atoi(v);
-  if (flags & AXONN_LB_NO_XSUM) xsum2 = 0;
+  if (flags & AXONN_LB_XSUM) xsum2 = 1;
   const bool reverse = (flags & AXONN_LB_REVERSE) != 0;
   auto members = [&](int r, int axis) {
     std::vector<int> m(g[axis]);

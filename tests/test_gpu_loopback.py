@@ -138,7 +138,7 @@ def _expected_paths(cfg, transposed, flags, grad_f32=False):
     ax_f, ax_b = (0, 1) if transposed else (1, 0)
     want = set()
     red2, no_x, pair = bool(flags & 1), bool(flags & 16), bool(flags & 32)
-    xs = not (flags & 256)
+    xs = bool(flags & 256)
 
     def two(name, es2=True):
         if pair and es2:
@@ -202,17 +202,16 @@ CASES = [(G, cfg) for G in (2, 3, 4, 6, 8) for cfg in grid.enumerate_configs(G)]
 @pytest.mark.parametrize("transposed", [False, True])
 @pytest.mark.parametrize("G,cfg", CASES, ids=[f"{c[0]}{c[1]}{c[2]}{c[3]}" for _, c in CASES])
 def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
-    # default 2-rank mode (the exchange summed inside the GEMM, kXSum: here
-    # the first rank of each pair leaves its sums to the sweep, the second
-    # sums in the epilogue) and the copy-engine AG_z; the exchange + local
-    # sum; multimem.red forced on 2-rank axes with the SM-pull AG_z; the
-    # 2-rank scatter + owner phase (exchange off)
-    nx = ax.AXONN_LB_NO_XSUM
+    # default 2-rank mode for these short K (exchange of whole partials) and
+    # the copy-engine AG_z; multimem.red forced on 2-rank axes with the
+    # SM-pull AG_z; the 2-rank scatter + owner phase (exchange off); the
+    # exchange summed inside the GEMM (kXSum, opt-in: here the first rank of
+    # each pair leaves its sums to the sweep, the second sums in the GEMM)
     check(ax, G, cfg, transposed, "int", 0)
-    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_REVERSE)
-    check(ax, G, cfg, transposed, "int", nx)
-    check(ax, G, cfg, transposed, "int", nx | ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
-    check(ax, G, cfg, transposed, "int", nx | ax.AXONN_LB_NO_EXCHANGE)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_XSUM)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_XSUM | ax.AXONN_LB_REVERSE)
     # the sum finished inside the epilogue (kPairSum), each rank of a pair in
     # both roles (the second arriver sums and writes both outputs)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_PAIRSUM)
@@ -227,8 +226,8 @@ def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
 @pytest.mark.parametrize("G,cfg", [(G, c) for G, c in CASES if G in (4, 6, 8)],
                          ids=[f"{c[0]}{c[1]}{c[2]}{c[3]}" for G, c in CASES if G in (4, 6, 8)])
 def test_every_grid_uniform_within_tolerance(ax, G, cfg, transposed):
-    check(ax, G, cfg, transposed, "uniform", 0)
-    check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)
+    check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_RED_ALWAYS)
+    check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_XSUM)
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 2, 1), (1, 1, 1, 2), (1, 1, 4, 2), (1, 1, 2, 4),
@@ -248,14 +247,12 @@ def test_emulated_multicast_agrees(ax, cfg):
     """Without a multicast object (red.global.add / plain stores) the results
     are the same bits (the stand-in is only used on devices without NVLS)."""
     G = int(np.prod(cfg))
-    check(ax, G, cfg, False, "int",
-          ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_EMULATE_MC | ax.AXONN_LB_NO_XSUM)
+    check(ax, G, cfg, False, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_EMULATE_MC)
 
 
 def test_multicast_object_used_when_available(ax):
     torch = require_cuda()
-    _, _, paths = run_loopback(ax, *SHAPES[2], (1, 2, 1, 1), False, "int",
-                               ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)
+    _, _, paths = run_loopback(ax, *SHAPES[2], (1, 2, 1, 1), False, "int", ax.AXONN_LB_RED_ALWAYS)
     print("loopback multicast object:", "multicast" in paths)
     assert "fwd_red" in paths   # normal layer: the forward all-reduce runs over Y
 
@@ -284,9 +281,10 @@ def test_long_k_tile_configuration(cfg):
         "import test_gpu_loopback as t, paper_2502_08145_b200 as ax\n"
         "for T in (False, True):\n"
         "    t.check(ax, %d, %r, T, 'int', 0)\n"
-        "    t.check(ax, %d, %r, T, 'int', ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)\n"
+        "    t.check(ax, %d, %r, T, 'int', ax.AXONN_LB_RED_ALWAYS)\n"
+        "    t.check(ax, %d, %r, T, 'int', ax.AXONN_LB_XSUM)\n"
         "print('MT2_OK')\n" % (ROOT, os.path.join(ROOT, "tests"), int(np.prod(cfg)), cfg,
-                               int(np.prod(cfg)), cfg))
+                               int(np.prod(cfg)), cfg, int(np.prod(cfg)), cfg))
     env = dict(os.environ, AXONN_PAIR_MT_FUSED="2")
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=600, cwd=ROOT)
@@ -300,7 +298,7 @@ FULL = [  # (name, h, m, grid, layers): tensor-parallel proxies of BASELINE C3/C
 ]
 
 
-@pytest.mark.parametrize("flags", [0, 256], ids=["xsum", "red_exchange"])
+@pytest.mark.parametrize("flags", [0, 256], ids=["red_exchange", "xsum"])
 @pytest.mark.parametrize("name,h,m,cfg,which", FULL, ids=[f[0] for f in FULL])
 def test_full_size_tensor_parallel(ax, name, h, m, cfg, which, flags):
     """Full-size GPT-block layers on tensor-parallel grids, every rank on this
@@ -407,9 +405,9 @@ def test_gelu_layer(ax, cfg, transposed):
     elementwise pass after the other forward modes; dGeLU before line 11."""
     G = int(np.prod(cfg))
     paths = check_act(ax, G, cfg, transposed, 0)
-    paths_x = check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_XSUM)
-    check_act(ax, G, cfg, transposed, ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_NO_XSUM)
-    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE | ax.AXONN_LB_NO_XSUM)
+    paths_x = check_act(ax, G, cfg, transposed, ax.AXONN_LB_XSUM)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_RED_ALWAYS)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE)
     ax_f = 0 if transposed else 1
     if cfg[ax_f] == 2:
-        assert "fwd_xsum" in paths and "fwd_exchange" in paths_x
+        assert "fwd_exchange" in paths and "fwd_xsum" in paths_x
