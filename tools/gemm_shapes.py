@@ -48,9 +48,10 @@ def operands(op, Mm, Nn, Kk, dev):
     return A, B, C
 
 
-def time_it(fn, reps, s):
+def time_it(fn, reps, s, warm=True):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fn()
+    if warm:
+        fn()
     e0.record(s)
     for _ in range(reps):
         fn()
@@ -66,6 +67,7 @@ def main():
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--label", default=os.environ.get("AB_LABEL", "default"))
     ap.add_argument("--only", default=None, help="comma-separated shape names")
+    ap.add_argument("--no-warm", action="store_true", help="no warm-up launch (ncu captures)")
     args = ap.parse_args()
     dev = "cuda"
     torch.cuda.set_device(0)
@@ -92,7 +94,7 @@ def main():
                 torch.matmul(A.t(), B, out=C)
         t_ax, t_cb = [], []
         for _ in range(args.rounds):
-            t_ax.append(time_it(ours, args.reps, s))
+            t_ax.append(time_it(ours, args.reps, s, not args.no_warm))
             if not args.no_cublas:
                 t_cb.append(time_it(cub, args.reps, s))
         fl = 2.0 * Mm * Nn * Kk

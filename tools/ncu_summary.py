@@ -31,8 +31,11 @@ SHAPE_NAMES = [f"{l}_{p}" for l in ("qkv", "proj", "fc1", "fc2") for p in ("fwd"
 def main(rep, out_md, traffic_json=None, pick=None):
     """pick="odd": keep launches 1, 3, 5, ... (tools/gemm_shapes.py --reps 1
     --rounds 1 runs each C2 shape twice: warm-up, then the measured launch)."""
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):  # an exported raw page (ncu -i REP --page raw --csv)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
     recs = []

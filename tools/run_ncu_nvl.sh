@@ -6,10 +6,15 @@
 #     only rewrites the same bytes; the barrier kernels run unprofiled.
 o=gpurun_out/ncu3; mkdir -p $o
 export CUDA_VISIBLE_DEVICES=0
-cmd="python tools/gemm_shapes.py --reps 1 --rounds 1 --no-cublas"
+cmd="python tools/gemm_shapes.py --reps 1 --rounds 1 --no-cublas --no-warm"
 $cmd > $o/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:gemm_bf16 -c 24 -o $o/prof $cmd > $o/ncu_full.log 2>&1
+ncu --set full --clock-control none -k regex:gemm_bf16 -c 12 -o $o/prof $cmd > $o/ncu_full.log 2>&1
 echo NCU_EXIT=$? >> $o/ncu_full.log
+# only the exported pages travel back (the report itself can exceed the 64 MiB return limit)
+ncu -i $o/prof.ncu-rep --page raw --csv > $o/prof_raw.csv 2>> $o/ncu_full.log
+ncu -i $o/prof.ncu-rep --page details --csv > $o/prof_details.csv 2>> $o/ncu_full.log
+ls -la $o >> $o/ncu_full.log
+rm -f $o/prof.ncu-rep
 unset CUDA_VISIBLE_DEVICES
 export MASTER_ADDR=127.0.0.1 MASTER_PORT=29811 WORLD_SIZE=2
 # rank 1 twice: once beside a plain run of rank 0 (if the harness makes one), once beside ncu
