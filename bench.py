@@ -220,6 +220,29 @@ def oracle_sample(h: int, m_sample: int, min_seconds: float):
     return flops / el / 1e12, threads, desc
 
 
+def torch_cpu_bf16_sample(h: int, m_sample: int, min_seconds: float):
+    """The same block's products with torch CPU bf16 matmuls (oneDNN, AMX where
+    the host has it): the CPU bf16 throughput BASELINE.md quotes beside the
+    oracle.  Returns (TFLOP/s, threads)."""
+    import torch
+    layers = block_layers(h, m_sample)
+    g = torch.Generator().manual_seed(42)
+    data = [(torch.rand(m, k, generator=g).bfloat16(), torch.rand(k, n, generator=g).bfloat16(),
+             torch.rand(m, n, generator=g).bfloat16()) for m, k, n, _ in layers]
+    flops, t0, reps = 0.0, time.perf_counter(), 0
+    while True:
+        for (X, W, dY), L in zip(data, layers):
+            X @ W
+            dY @ W.t()
+            X.t() @ dY
+            flops += model_flops([L])
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or reps >= 50:
+            break
+    return flops / el / 1e12, torch.get_num_threads()
+
+
 def run_reference(args):
     """--impl reference: the oracle as it stands, on the host cores, rank 0 only,
     on a bounded sample of the primary workload of this GPU count."""
@@ -889,6 +912,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, thr, desc = oracle_sample(HIDDEN[spec["model"]], 2048, 10.0)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": desc}
+        try:
+            tv, tthr = torch_cpu_bf16_sample(HIDDEN[spec["model"]], 2048, 5.0)
+            cpu["torch_cpu_bf16"] = {"value": tv, "unit": "TFLOP/s", "threads": tthr,
+                                     "sample": "torch CPU bf16 matmuls of the same block products, "
+                                               "2048 token rows"}
+        except Exception as e:  # pragma: no cover
+            cpu["torch_cpu_bf16"] = {"error": str(e)[:200]}
 
     if rank == 0:
         value = prim["value"]
