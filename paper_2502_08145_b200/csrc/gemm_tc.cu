@@ -510,6 +510,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
   // Both are no-ops without the launch attribute.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // kLoadAll: the epilogue warpgroups take registers from warpgroup 0
+  // (producer, MMA issuer, helpers) within the CTA's launch allocation of
+  // 384 x 168: 128 x 56 + 256 x 224 = 64512 (setmaxnreg.inc would wait
+  // forever for registers the CTA does not have, so the host only launches
+  // this variant when the kernel was compiled to 168 registers)
+  constexpr bool kLoadAll = MT == 2 && !OUTF && DEEP;
 
   // kExchange / kXSum: the call counter picks the receive set (device-side
   // double buffering); kXSum: the flag epoch of this call
@@ -544,6 +550,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
     if (lane == 0) reinterpret_cast<int*>(epi.peer[5])[uu] = xepoch;
   };
 
+  if (warp < 4) {
+  // warpgroup 0: producer, MMA issuer, helpers (kLoadAll: 56 registers each;
+  // the CTA keeps its launch allocation, 384 x 168: 128 x 56 + 256 x 224)
+  if constexpr (kLoadAll) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
@@ -715,7 +725,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  }
+  } else {
+    // warpgroups 1 and 2: the epilogue (kLoadAll: 224 registers each)
+    if constexpr (kLoadAll) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
     // ------------------------------------------------ epilogue (both CTAs)
     // TMEM -> registers (thread = row) -> bf16 -> XOR-swizzled smem -> 16-B
     // vectors with 8 consecutive threads covering one 128-B row segment, so
@@ -758,34 +771,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
           while (ld_acquire_gpu(ready) == 0) __nanosleep(100);
         __syncwarp();
       }
-#pragma unroll 1
-      for (int mt = 0; mt < MT; ++mt) {
-        const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
-        const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
-        if (role == kRoleHead) {
-          // contributor: fp32 partial sums of K-blocks [0, h) to the workspace
-#pragma unroll 1
-          for (int q = 0; q < 4; ++q) {
-            uint32_t v[32];
-            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
-                                        static_cast<uint32_t>(chalf * 128 + q * 32),
-                                    v);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *ws_unit(mt, q, j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-          }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0 && (MT == 2 || mt == MT - 1)) ptx::mbar_arrive_leader(&tempty[MT == 2 ? mt : acc]);
-          continue;
-        }
-        // bf16: this warp's share of sub-tile mt goes TMEM -> registers (RNE-packed)
-        // first and the sub-tile is released at once, so the MMA warp resumes
-        // before the staging and stores below
-        uint32_t pk[OUTF ? 1 : NCH][32];
+      // bf16: this warp's share of sub-tile mt goes TMEM -> registers
+      // (RNE-packed; + the stream-K partial sums on a TAIL) and the sub-tile
+      // is released at once, so the MMA warp resumes before the staging and
+      // stores.  kLoadAll (the 4-stage 512x256 pipeline): both sub-tiles are
+      // loaded and released before any store (the epilogue warps hold 128
+      // packed registers; setmaxnreg above), so the next tile's MMAs never
+      // wait for sub-tile 0's stores.
+      auto load_pack = [&](int mt, uint32_t (&pkd)[OUTF ? 1 : NCH][32]) {
         if constexpr (!OUTF) {
+          const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
 #pragma unroll
           for (int ci = 0; ci < NCH; ++ci) {
             uint32_t v0[32], v1[32];
@@ -811,14 +806,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
             }
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              pk[ci][i] = ptx::pack_bf16x2(v0[2 * i], v0[2 * i + 1]);
-              pk[ci][16 + i] = ptx::pack_bf16x2(v1[2 * i], v1[2 * i + 1]);
+              pkd[ci][i] = ptx::pack_bf16x2(v0[2 * i], v0[2 * i + 1]);
+              pkd[ci][16 + i] = ptx::pack_bf16x2(v1[2 * i], v1[2 * i + 1]);
             }
           }
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_leader(&tempty[MT == 2 ? mt : acc]);
         }
+      };
+      uint32_t pkall[kLoadAll ? 2 : 1][OUTF ? 1 : NCH][32];
+      if constexpr (kLoadAll) {
+        if (role != kRoleHead) {
+          load_pack(0, pkall[0]);
+          load_pack(1, pkall[1]);
+        }
+      }
+#pragma unroll (kLoadAll ? 2 : 1)
+      for (int mt = 0; mt < MT; ++mt) {
+        const int row0 = tc.m0 + Cfg::ROWS_CTA * static_cast<int>(rank) + 128 * mt + 32 * e;
+        const uint32_t col_base = static_cast<uint32_t>((acc * MT + mt) * Cfg::BN);
+        if (role == kRoleHead) {
+          // contributor: fp32 partial sums of K-blocks [0, h) to the workspace
+#pragma unroll 1
+          for (int q = 0; q < 4; ++q) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + col_base +
+                                        static_cast<uint32_t>(chalf * 128 + q * 32),
+                                    v);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *ws_unit(mt, q, j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0 && (MT == 2 || mt == MT - 1)) ptx::mbar_arrive_leader(&tempty[MT == 2 ? mt : acc]);
+          continue;
+        }
+        uint32_t pk_one[OUTF ? 1 : NCH][32];
+        if constexpr (!kLoadAll) load_pack(mt, pk_one);
+        uint32_t(&pk)[OUTF ? 1 : NCH][32] = kLoadAll ? pkall[kLoadAll ? mt : 0] : pk_one;
 #pragma unroll (OUTF ? 1 : NCH)
         for (int ci = 0; ci < NCH; ++ci) {
           const int c = chalf * NCH + ci;
@@ -1260,7 +1289,12 @@ cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb,
                            const CUtensorMap& mc, int use_tma_store, void* C, int64_t ldc, int M,
                            int N, int K, int num_sms, int group_m, const EpiTarget& epi,
                            cudaStream_t stream) {
-  static const bool deep = env_int("AXONN_MT2_DEEP", 1) != 0;
+  // the deep variant's register hand-over assumes 168 registers per thread
+  static const bool deep = env_int("AXONN_MT2_DEEP", 1) != 0 && [] {
+    cudaFuncAttributes fa;
+    return cudaFuncGetAttributes(&fa, gemm_bf16_tcgen05_pair<A_MN, B_MN, 2, 0, 1>) == cudaSuccess &&
+           fa.numRegs == 168;
+  }();
   if (mt == 2)
     return deep ? launch_pair<A_MN, B_MN, 2, 0, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
                                                    num_sms, group_m, epi, stream)
