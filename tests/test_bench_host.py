@@ -1,0 +1,52 @@
+"""Host-side pieces of bench.py that need no GPU: the Chrome-trace writer
+(--trace) and the block / chain plans it labels."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+class FakeEvent:
+    """Stands in for torch.cuda.Event: a timestamp in ms."""
+
+    def __init__(self, t_ms):
+        self.t = t_ms
+
+    def elapsed_time(self, other):
+        return other.t - self.t
+
+
+def test_trace_is_valid_chrome_trace(tmp_path):
+    base = FakeEvent(0.0)
+    nrep = 2
+    # two layer phases and the sync, each rep: [start, end] pairs
+    ev = {"qkv_fwd": [FakeEvent(1.0), FakeEvent(1.5), FakeEvent(10.0), FakeEvent(10.5)],
+          "qkv_fwd_gemm": [FakeEvent(2.0), FakeEvent(2.4), FakeEvent(11.0), FakeEvent(11.4)],
+          "sync": [FakeEvent(3.0), FakeEvent(3.01), FakeEvent(12.0), FakeEvent(12.01)]}
+    path = tmp_path / "trace.json"
+    bench.write_trace(str(path), None, ev, base, nrep, {"label": "C3 proxy", "grid": (2, 2, 1, 1)})
+    d = json.load(open(path))
+    evs = [e for e in d["traceEvents"] if e["ph"] == "X"]
+    assert len(evs) == 3 * nrep
+    assert any(e["ph"] == "M" and e["args"]["name"] == "rank 0" for e in d["traceEvents"])
+    by = {(e["name"], e["args"]["rep"]): e for e in evs}
+    # microseconds relative to the base event, durations from the pairs
+    assert by[("qkv_fwd", 0)]["ts"] == 1000.0 and by[("qkv_fwd", 0)]["dur"] == 500.0
+    assert by[("qkv_fwd", 1)]["ts"] == 10000.0
+    assert by[("qkv_fwd_gemm", 1)]["cat"] == "gemm_only"
+    assert by[("sync", 0)]["cat"] == "sync" and by[("qkv_fwd", 0)]["cat"] == "alg1"
+    assert d["otherData"]["grid"] == [2, 2, 1, 1]
+
+
+def test_block_layers_phases():
+    a = bench.block_layers(4096, 16384, "A")
+    b = bench.block_layers(4096, 16384, "B")
+    assert [t for *_, t in a] == [False, True, False, True]
+    assert [t for *_, t in b] == [True, False, True, False]
+    # Table II shapes: QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h
+    assert [(k, n) for _, k, n, _ in a] == [(4096, 12288), (4096, 4096), (4096, 16384), (16384, 4096)]
+    assert bench.model_flops(a) == sum(6 * 16384 * k * n for _, k, n, _ in a)
