@@ -27,6 +27,16 @@
 namespace axonn {
 namespace {
 
+// Programmatic dependent launch for the small kernels between the GEMMs
+// (barriers, owner phases, gathers, waits): launched early when the previous
+// kernel in the stream allows it, they wait for its completion before any
+// memory access and let the next kernel be scheduled at once.  No-ops
+// without the launch attribute (AXONN_PDL=0).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void k_mc_ptr(ncclWindow_t w, ncclDevComm dc, void** out) {
   out[0] = ncclGetLsaMultimemPointer(w, 0, dc);
   out[1] = ncclGetLocalPointer(w, 0);
@@ -74,6 +84,7 @@ template <bool F32>
 __global__ void k_owner_reduce(const uint4* __restrict__ recv0, const uint4* __restrict__ recv1,
                                const int* __restrict__ par, long long n16, int P,
                                const __grid_constant__ OwnerOut out) {
+  pdl_enter();
   constexpr int UNIT = F32 ? 4 : 8;  // elements per 16-B unit
   // kExchange double buffering: the barrier before this kernel advanced the
   // parity counter past the value the producing GEMM read
@@ -142,6 +153,7 @@ struct PullSrc {
   const uint4* p[8];
 };
 __global__ void k_gather_pull(PullSrc src, int P, long long n16, uint4* __restrict__ dst) {
+  pdl_enter();
   const long long total = static_cast<long long>(P) * n16;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
@@ -156,6 +168,7 @@ __global__ void k_gather_pull(PullSrc src, int P, long long n16, uint4* __restri
 // count.  A bounded spin: a lost chunk traps (a launch error) instead of
 // hanging the device.
 __global__ void k_pair_wait(const uint32_t* done, uint32_t* calls, uint32_t total) {
+  pdl_enter();
   if (threadIdx.x != 0) return;
   const uint32_t c = *calls;
   const uint32_t target = (c + 1u) * total;
@@ -174,6 +187,7 @@ __global__ void k_pair_wait(const uint32_t* done, uint32_t* calls, uint32_t tota
 __global__ void k_xsum_sweep(const char* __restrict__ recv0, const char* __restrict__ recv1,
                              char* __restrict__ out, int* ctrl, int M, int N, long long U,
                              int* calls, unsigned* fin) {
+  pdl_enter();
   const int c = *reinterpret_cast<volatile int*>(calls);
   const int epoch = c + 1;
   const char* s0 = (c & 1) ? recv1 : recv0;
@@ -231,6 +245,7 @@ __global__ void k_xsum_sweep(const char* __restrict__ recv0, const char* __restr
 }
 
 __global__ void k_barrier(ncclDevComm dc, uint32_t index, int* ctr) {
+  pdl_enter();
   ncclLsaBarrierSession<ncclCoopCta> b(ncclCoopCta(), dc, ncclTeamTagLsa(), index);
   b.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   // kExchange parity: the next call's epilogue targets the other buffers
@@ -238,6 +253,25 @@ __global__ void k_barrier(ncclDevComm dc, uint32_t index, int* ctr) {
 }
 
 }  // namespace
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                       Args... args) {
+  static const bool pdl = [] {
+    const char* v = std::getenv("AXONN_PDL");
+    return !(v && std::atoi(v) == 0);
+  }();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(block);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+}
 
 struct SymAxisImpl {
   ncclComm_t comm = nullptr;
@@ -398,10 +432,8 @@ cudaError_t sym_owner_reduce(const void* recv, long long slice, int P, bool f32,
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
   if (blocks < 1) blocks = 1;
   auto kern = f32 ? k_owner_reduce<true> : k_owner_reduce<false>;
-  kern<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-      reinterpret_cast<const uint4*>(recv), reinterpret_cast<const uint4*>(recv_alt ? recv_alt : recv),
-      par, n16, P, out);
-  return cudaGetLastError();
+  return launch_pdl(kern, static_cast<unsigned>(blocks), 256, st, reinterpret_cast<const uint4*>(recv),
+                    reinterpret_cast<const uint4*>(recv_alt ? recv_alt : recv), par, n16, P, out);
 }
 
 cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* dst,
@@ -494,15 +526,13 @@ cudaError_t sym_gather_pull(const void* const* src, int P, size_t bytes, void* d
   long long blocks = (P * n16 + 255) / 256;
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
   if (blocks < 1) blocks = 1;
-  k_gather_pull<<<static_cast<unsigned>(blocks), 256, 0, st>>>(ps, P, n16,
-                                                               static_cast<uint4*>(dst));
-  return cudaGetLastError();
+  return launch_pdl(k_gather_pull, static_cast<unsigned>(blocks), 256, st, ps, P, n16,
+                    static_cast<uint4*>(dst));
 }
 
 cudaError_t sym_pair_wait(const void* done, void* calls, uint32_t total, cudaStream_t st) {
-  k_pair_wait<<<1, 32, 0, st>>>(static_cast<const uint32_t*>(done), static_cast<uint32_t*>(calls),
-                                total);
-  return cudaGetLastError();
+  return launch_pdl(k_pair_wait, 1, 32, st, static_cast<const uint32_t*>(done),
+                    static_cast<uint32_t*>(calls), total);
 }
 
 cudaError_t sym_xsum_sweep(const void* recv0, const void* recv1, void* out, void* ctrl,
@@ -512,16 +542,15 @@ cudaError_t sym_xsum_sweep(const void* recv0, const void* recv1, void* out, void
   char* c = static_cast<char*>(ctrl);
   long long blocks = (U + 7) / 8;
   if (blocks > 2LL * num_sms) blocks = 2LL * num_sms;
-  k_xsum_sweep<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-      static_cast<const char*>(recv0), static_cast<const char*>(recv1), static_cast<char*>(out),
-      reinterpret_cast<int*>(c), static_cast<int>(rows), static_cast<int>(cols), U,
-      reinterpret_cast<int*>(c + xsum_calls_off(U)), reinterpret_cast<unsigned*>(c + xsum_fin_off(U)));
-  return cudaGetLastError();
+  return launch_pdl(k_xsum_sweep, static_cast<unsigned>(blocks), 256, st,
+                    static_cast<const char*>(recv0), static_cast<const char*>(recv1),
+                    static_cast<char*>(out), reinterpret_cast<int*>(c), static_cast<int>(rows),
+                    static_cast<int>(cols), U, reinterpret_cast<int*>(c + xsum_calls_off(U)),
+                    reinterpret_cast<unsigned*>(c + xsum_fin_off(U)));
 }
 
 cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index, int* ctr) {
-  k_barrier<<<1, 32, 0, st>>>(a->impl->dev, static_cast<uint32_t>(index), ctr);
-  return cudaGetLastError();
+  return launch_pdl(k_barrier, 1, 32, st, a->impl->dev, static_cast<uint32_t>(index), ctr);
 }
 
 }  // namespace axonn

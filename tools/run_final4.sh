@@ -1,0 +1,10 @@
+#!/bin/bash
+# 4-GPU validation: multi-GPU parity suite, then the N=2 and N=4 bench lines
+# (with their sub-records), a Chrome trace, and the per-layer phases.
+o=gpurun_out/f4; mkdir -p $o
+tr() { python -m torch.distributed.run --nnodes=1 --nproc-per-node $1 --master-addr 127.0.0.1 --master-port $2 "${@:3}"; }
+timeout 2400 python -m pytest tests/test_gpu_multi.py -q -rs > $o/pt_multi.log 2>&1; echo EXIT=$? >> $o/pt_multi.log
+for n in 2 4; do
+  timeout 900 bash -c "$(declare -f tr); tr $n 2990$n bench.py --gpus $n --steps 20 --warmup 5 --trace $o/trace_N$n.json" > $o/bench_N$n.json 2> $o/bench_N$n.err
+done
+timeout 600 bash -c "$(declare -f tr); tr 4 29911 tools/layer_phases.py --model 20B --tokens 8192 --grid 2,2,1,1 --out $o/phases_c3proxy_N4.json" > $o/phases.log 2>&1
