@@ -277,9 +277,13 @@ enum {
   AXONN_LB_PAIRPULL = 128,   /* with AXONN_LB_PAIRSUM: each rank keeps its partial
                                 in its own receive buffer and the second
                                 arriver reads the peer's over NVLink (pull)   */
-  AXONN_LB_XSUM = 256        /* 2-rank bf16 axes at every K: the exchange summed
+  AXONN_LB_XSUM = 256,       /* 2-rank bf16 axes at every K: the exchange summed
                                 inside the GEMM (kXSum, AXONN_XSUM=1 on the
                                 multi-GPU path; opt-in, measured slower)      */
+  AXONN_LB_SIDESUM = 512     /* the backward's 2-rank exchange of dÎ summed by the
+                                dW GEMM's helper warps instead of a separate
+                                pass (AXONN_SIDESUM=1 on the multi-GPU path;
+                                opt-in, measured no faster)                   */
 };
 enum {
   AXONN_LB_PATH_FWD_RED = 1, AXONN_LB_PATH_FWD_SCATTER = 2,
@@ -294,7 +298,8 @@ enum {
   AXONN_LB_PATH_FWD_PAIRSUM = 16384, AXONN_LB_PATH_BWD_PAIRSUM = 32768,
   AXONN_LB_PATH_DP_PAIRSUM = 65536,
   AXONN_LB_PATH_FWD_XSUM = 131072, AXONN_LB_PATH_BWD_XSUM = 262144,
-  AXONN_LB_PATH_DP_XSUM = 524288
+  AXONN_LB_PATH_DP_XSUM = 524288,
+  AXONN_LB_PATH_BWD_SIDESUM = 1048576  /* dÎ's exchange summed inside the dW GEMM */
 };
 axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
                                    const void* const* I_local, const void* const* W_hat,

@@ -187,7 +187,8 @@ axonn_status_t check_async_nccl() {
 // One local product on `st`, instrumented.  K == 0 writes zeros.
 axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                         int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                        cudaStream_t st, const axonn::EpiTarget* epi = nullptr) {
+                        cudaStream_t st, const axonn::EpiTarget* epi = nullptr,
+                        const axonn::SideSum* side = nullptr) {
   STATUS_TRY(ensure_device());
   if (M == 0 || N == 0) return AXONN_OK;
   const size_t es = dtype == AXONN_BF16_GRADF32 ? 4 : elem_size(dtype);  // of C
@@ -223,7 +224,7 @@ axonn_status_t run_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, cons
   axonn::GemmStatus gs;
   if (dtype == AXONN_BF16 || dtype == AXONN_BF16_GRADF32)
     gs = axonn::gemm_bf16_tc(op, M, N, K, A, lda, B, ldb, C, ldc, S.gemm_sms, st, epi,
-                             dtype == AXONN_BF16_GRADF32);
+                             dtype == AXONN_BF16_GRADF32, side);
   else
     gs = axonn::gemm_f32_simt(op, M, N, K, static_cast<const float*>(A), lda,
                               static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc, st);
@@ -336,7 +337,9 @@ struct axonn_fc {
     axonn::SymBuf recv;   // P-rank scatter mode: P slots of elems / P; exchange: P slots of elems
     axonn::SymBuf recv2;  // exchange mode: the second receive buffer (device-side parity)
     int* par = nullptr;   // exchange mode: parity counter, advanced by the post barrier
-    axonn::SymBuf ctrl;   // pair-sum mode: arbitration tickets + done / call counters
+    axonn::SymBuf ctrl;   // pair-sum mode: arbitration tickets + done / call counters;
+                          // exchange mode: the side-sum words (arrive, go, finished)
+    int* side_arrive_peer = nullptr;  // exchange mode: the peer's arrive word (LSA)
     long long chunks = 0; // pair-sum mode: 32 x 64 output chunks
     int64_t cols = 0;     // row length of the reduced output
     axonn::EpiTarget epi;
@@ -426,6 +429,7 @@ void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_
     const int P = S.g[axis];
     reqs->push_back({axis, f->elems * es * P, &f->recv});
     reqs->push_back({axis, f->elems * es * P, &f->recv2});
+    reqs->push_back({axis, 256, &f->ctrl});  // side-sum words (SideSum)
   }
 }
 
@@ -518,6 +522,14 @@ bool fused_bind(axonn_fc::Fused* f, std::string* why) {
       return false;
     }
     f->epi = axonn::epi_exchange(P, me, static_cast<long long>(f->elems), peer, alt, f->par);
+    if (P == 2 && f->ctrl.ptr) {
+      f->side_arrive_peer = static_cast<int*>(axonn::sym_peer_ptr(&f->ctrl, 1 - me));
+      if (!f->side_arrive_peer || cudaMemset(f->ctrl.ptr, 0, 256) != cudaSuccess ||
+          cudaDeviceSynchronize() != cudaSuccess) {
+        *why = "exchange side-sum words unavailable";
+        return false;
+      }
+    }
     return true;
   }
   f->epi = axonn::epi_scatter(P, me, static_cast<long long>(f->elems) / P, peer);
@@ -562,6 +574,7 @@ void fused_reset(axonn_fc::Fused* f) {
   f->par = nullptr;
   f->epi = axonn::EpiTarget();
   f->out_peer = nullptr;
+  f->side_arrive_peer = nullptr;
   f->elems = 0;
 }
 
@@ -701,8 +714,8 @@ axonn_status_t apply_act(axonn_fc* h, void* O_local, cudaStream_t st) {
 namespace axonn {
 axonn_status_t rt_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                        int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                       cudaStream_t st, const EpiTarget* epi) {
-  return run_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, st, epi);
+                       cudaStream_t st, const EpiTarget* epi, const SideSum* side) {
+  return run_gemm(op, dtype, M, N, K, A, lda, B, ldb, C, ldc, st, epi, side);
 }
 axonn_status_t rt_fail(axonn_status_t s, const char* msg) { return fail(s, "%s", msg); }
 void rt_count_launch() { g_launches.fetch_add(1); }
@@ -1158,6 +1171,27 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     return run_gemm(AXONN_OP_NT, adt, g.m_l, g.k_l, g.n_l, dO_local, g.n_l, h->W, g.n_l,
                     fI ? h->fi.out.ptr : dI_local, g.k_l, st, fI ? &h->fi.epi : nullptr);
   };
+  // line 12's local sum inside line 13's GEMM (opt-in, AXONN_SIDESUM=1): a
+  // 2-rank exchange of dÎ is summed by the dW GEMM's idle helper warps beside
+  // its tiles (SideSum), so no barrier kernel and no pass over dI follow the
+  // dW GEMM (measured: the GEMM slows by about what the pass cost)
+  axonn::SideSum side;
+  const bool side_on = fI && h->fi.epi.mode == axonn::kExchange && h->fi.epi.P == 2 &&
+                       h->fi.side_arrive_peer && h->fi.par && env_int("AXONN_SIDESUM", 0) != 0 &&
+                       g.k_l > 0 && g.n_l > 0 && g.m_l > 0 &&
+                       !(fW && h->fw.epi.mode == axonn::kXSum);
+  if (side_on) {
+    char* c = static_cast<char*>(h->fi.ctrl.ptr);
+    side.recv0 = h->fi.recv.ptr;
+    side.recv1 = h->fi.recv2.ptr;
+    side.out = h->fi.out.ptr;
+    side.n16 = static_cast<long long>(h->fi.elems * h->fi.es / 16);
+    side.par = h->fi.par;
+    side.arrive_own = reinterpret_cast<int*>(c);
+    side.arrive_peer = h->fi.side_arrive_peer;
+    side.go = reinterpret_cast<int*>(c + 64);
+    side.fin = reinterpret_cast<unsigned*>(c + 128);
+  }
   // line 13: dW partial = I^T x dO  (M = k_l, N = n_l, K = m_l)
   auto dW_gemm = [&]() -> axonn_status_t {
     // the previous RS_z of this layer must be done with its source: the
@@ -1165,7 +1199,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     // the NCCL one's read of dwpart (write-after-read race)
     if (rs) CUDA_TRY(wait_xcall(st, h->ev_rsdone));
     return run_gemm(AXONN_OP_TN, dt, g.k_l, g.n_l, g.m_l, h->I, g.k_l, dO_local, g.n_l, dst, g.n_l,
-                    st, fW ? &h->fw.epi : (fZ ? &h->fz.epi : nullptr));
+                    st, fW ? &h->fw.epi : (fZ ? &h->fz.epi : nullptr), side_on ? &side : nullptr);
   };
   // line 14 (ORS, waited in grads_sync) and the per-layer data-parallel sum
   auto grad_comm = [&]() -> axonn_status_t {
@@ -1259,8 +1293,9 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     STATUS_TRY(dI_gemm());
   }
   if (fW) count_comm(4, S.g[AX_D], S_el, gdt);
-  // fused dI: every rank's reductions have landed after this
-  if (fI) STATUS_TRY(fused_post(h->fi, st));
+  // fused dI: every rank's reductions have landed after this (side_on: the
+  // dW GEMM summed them)
+  if (fI && !side_on) STATUS_TRY(fused_post(h->fi, st));
   if (fI && dI_local != h->fi.out.ptr)
     CUDA_TRY(cudaMemcpyAsync(dI_local, h->fi.out.ptr, static_cast<size_t>(g.m_l * g.k_l) * es,
                              cudaMemcpyDeviceToDevice, st));

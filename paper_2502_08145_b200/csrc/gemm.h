@@ -57,13 +57,35 @@ struct EpiTarget {
 enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4, kPairSum = 5,
                kXSum = 6 };
 
+// A memory-bound task the GEMM's idle helper warps (2 and 3 of every CTA)
+// run beside its tiles: the local sum of a 2-rank exchange all-reduce whose
+// partials a PREVIOUS GEMM left in this rank's receive set (slot 0 + slot 1
+// in fp32, one RNE rounding -> out; the backward's dI sum run inside the dW
+// GEMM that follows it, Alg. 1 lines 12-13).  Cross-rank: one CTA raises
+// the peer's arrive word to epoch p + 1 (p = *par at kernel start: the set
+// the producing GEMM used) and waits for its own, then opens `go` for the
+// helpers; the last helper warp out advances *par.  arrive_peer == null: no
+// barrier (the single-GPU loopback, where stream order stands in for it).
+struct SideSum {
+  const void* recv0 = nullptr;  // this rank's receive sets: 2 slots of n16 16-B units each
+  const void* recv1 = nullptr;
+  void* out = nullptr;
+  long long n16 = 0;            // 0: no side task
+  int* par = nullptr;
+  int* arrive_own = nullptr;    // raised by the peer
+  int* arrive_peer = nullptr;   // the peer's (NVLink) arrive word
+  int* go = nullptr;
+  unsigned* fin = nullptr;
+};
+
 enum class GemmStatus { kOk = 0, kBadShape, kBadAlignment, kTensorMap, kBadOp, kLaunch };
 
 // bf16 x bf16 -> bf16 (fp32 accumulate) on tcgen05; op 0 = NN, 1 = NT, 2 = TN.
 // out_f32: C is fp32 (op 2 only: the dW product of fp32 gradient reduction).
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream, const EpiTarget* epi = nullptr, bool out_f32 = false);
+                        cudaStream_t stream, const EpiTarget* epi = nullptr, bool out_f32 = false,
+                        const SideSum* side = nullptr);
 
 // The launch error behind the last GemmStatus::kLaunch on this thread (the
 // launch helpers consume cudaGetLastError()).

@@ -337,6 +337,12 @@ __device__ __forceinline__ int ld_acquire_sys_i(const int* p) {
 __device__ __forceinline__ void st_relaxed_sys_i(int* p, int v) {
   asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint4 ldcg_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ float4 ld_cg_f4(const float4* p) {  // L2 only: written by another SM
   float4 v;
   asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -383,7 +389,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
                            void* __restrict__ Cv, int64_t ldc, int M, int N, int K,
                            int split_release,
                            int group_m, const __grid_constant__ EpiTarget epi,
-                           int* __restrict__ tile_counter, const __grid_constant__ SkParams sk) {
+                           int* __restrict__ tile_counter, const __grid_constant__ SkParams sk,
+                           const __grid_constant__ SideSum side) {
   using Cfg = PairCfg<MT, DEEP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -516,6 +523,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
   // forever for registers the CTA does not have, so the host only launches
   // this variant when the kernel was compiled to 168 registers)
   constexpr bool kLoadAll = MT == 2 && !OUTF && DEEP;
+  // side task (SideSum): the epoch of this call, read before any CTA can
+  // have advanced it (the last helper warp out does, after every CTA started)
+  const int side_p = side.n16 > 0 ? *reinterpret_cast<const volatile int*>(side.par) : 0;
 
   // kExchange / kXSum: the call counter picks the receive set (device-side
   // double buffering); kXSum: the flag epoch of this call
@@ -684,6 +694,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
     }
     __syncwarp();
   } else if (warp == 2 || warp == 3) {
+    if (side.n16 > 0) {
+      // ---------------------------------------------- side task (SideSum)
+      const int want = side_p + 1;
+      if (blockIdx.x == 0 && warp == 3 && lane == 0) {  // CTA 0 meets the peer
+        if (side.arrive_peer) {
+          // our previous kernels' writes to the peer (the producing GEMM's
+          // partial) happen before this release; the peer's before our acquire
+          asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(side.arrive_peer), "r"(want)
+                       : "memory");
+          long long spins = 0;
+          while (ld_acquire_sys_i(side.arrive_own) - want < 0) {
+            __nanosleep(128);
+            if (++spins > (1LL << 27)) __trap();  // the peer never arrived: fail loudly
+          }
+        }
+        st_release_gpu(side.go, want);
+      }
+      if (lane == 0)
+        while (ld_acquire_gpu(side.go) - want < 0) __nanosleep(256);
+      __syncwarp();
+      const uint4* r = reinterpret_cast<const uint4*>((side_p & 1) ? side.recv1 : side.recv0);
+      uint4* o = reinterpret_cast<uint4*>(side.out);
+      const long long n16 = side.n16;
+      const long long stride = static_cast<long long>(gridDim.x) * 64;
+      long long i = static_cast<long long>(blockIdx.x) * 64 + (warp - 2) * 32 + lane;
+      for (; i + 3 * stride < n16; i += 4 * stride) {  // 8 loads in flight per thread
+        uint4 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = ldcg_u4(r + i + u * stride);
+          b[u] = ldcg_u4(r + n16 + i + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[i + u * stride] = ptx::add_bf16x8(a[u], b[u]);
+      }
+      for (; i < n16; i += stride) o[i] = ptx::add_bf16x8(ldcg_u4(r + i), ldcg_u4(r + n16 + i));
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(side.fin, 1u) == 2 * gridDim.x - 1) {  // every helper warp is done
+          *side.fin = 0;
+          *side.par = want;  // the producing GEMM's next call takes the other receive set
+          __threadfence();
+        }
+      }
+    }
     // ------------------------------------------------ kXSum helpers (both CTAs)
     // Helper c sums ring slots c, c + 2, ... in order once the peer's flag for
     // the unit is up.  It never holds the epilogue back for long: when the
@@ -1247,7 +1303,8 @@ SkParams stream_k_plan(int tiles, int pairs, int num_kb, int mt, cudaStream_t st
 template <int A_MN, int B_MN, int MT, int OUTF = 0, int DEEP = 0>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                         int use_tma_store, void* C, int64_t ldc, int M, int N, int K, int num_sms,
-                        int group_m, const EpiTarget& epi, cudaStream_t stream) {
+                        int group_m, const EpiTarget& epi, cudaStream_t stream,
+                        const SideSum& side = SideSum()) {
   using Cfg = PairCfg<MT, DEEP>;
   auto kern = gemm_bf16_tcgen05_pair<A_MN, B_MN, MT, OUTF, DEEP>;
   static bool attr_set = false;
@@ -1279,7 +1336,7 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&lc, kern, ma, mb, mc, use_tma_store, C, ldc, M, N, K, split, group_m,
-                            epi, counter, sk);
+                            epi, counter, sk, side);
 }
 
 // MT = 2 takes the deep-pipeline configuration (4 operand stages, one
@@ -1288,7 +1345,7 @@ template <int A_MN, int B_MN>
 cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb,
                            const CUtensorMap& mc, int use_tma_store, void* C, int64_t ldc, int M,
                            int N, int K, int num_sms, int group_m, const EpiTarget& epi,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const SideSum& side) {
   // the deep variant's register hand-over assumes 168 registers per thread
   static const bool deep = env_int("AXONN_MT2_DEEP", 1) != 0 && [] {
     cudaFuncAttributes fa;
@@ -1297,11 +1354,11 @@ cudaError_t launch_pair_mt(int mt, const CUtensorMap& ma, const CUtensorMap& mb,
   }();
   if (mt == 2)
     return deep ? launch_pair<A_MN, B_MN, 2, 0, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
-                                                   num_sms, group_m, epi, stream)
+                                                   num_sms, group_m, epi, stream, side)
                 : launch_pair<A_MN, B_MN, 2, 0, 0>(ma, mb, mc, use_tma_store, C, ldc, M, N, K,
-                                                   num_sms, group_m, epi, stream);
+                                                   num_sms, group_m, epi, stream, side);
   return launch_pair<A_MN, B_MN, 1>(ma, mb, mc, use_tma_store, C, ldc, M, N, K, num_sms, group_m,
-                                    epi, stream);
+                                    epi, stream, side);
 }
 
 int env_int(const char* name, int dflt) {
@@ -1320,7 +1377,9 @@ thread_local cudaError_t g_launch_error = cudaSuccess;
 // 256x256 for shorter fused launches.  AXONN_GROUP_M sets the raster band.
 GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* C, int64_t ldc, int num_sms,
-                        cudaStream_t stream, const EpiTarget* epi_in, bool out_f32) {
+                        cudaStream_t stream, const EpiTarget* epi_in, bool out_f32,
+                        const SideSum* side_in) {
+  const SideSum side = side_in ? *side_in : SideSum();
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return GemmStatus::kBadShape;
   if ((lda & 7) || (ldb & 7) || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
@@ -1329,7 +1388,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
     const char* v = std::getenv("AXONN_GEMM_VARIANT");
     return v && std::strcmp(v, "single") == 0;
   }();
-  const bool single = single_env && !out_f32;  // the 1-CTA kernel has no fp32 epilogue
+  // the 1-CTA kernel has no fp32 epilogue and no side task
+  const bool single = single_env && !out_f32 && !(side_in && side_in->n16 > 0);
   // raster band: 4096 rows of tiles (AXONN_GROUP_M overrides, in tiles; < 0 = bands of N tiles)
   static const int group_m_env = env_int("AXONN_GROUP_M", 0);
   // 512x256 tiles (MT=2: less L2/DRAM traffic per flop) for plain-store
@@ -1373,6 +1433,8 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
     return GemmStatus::kBadAlignment;
   if (epi.mode == kXSum && (out_f32 || ldc != N || epi.slice != M * N || epi.P != 2 || !epi.par))
     return GemmStatus::kBadAlignment;
+  if (side.n16 > 0 && (epi.mode == kXSum || !side.par || !side.go || !side.fin || !side.out))
+    return GemmStatus::kBadAlignment;  // the helper warps run one task; the task needs its state
   if (epi.mode == kPairSum && (out_f32 || ldc != N || epi.slice != (N + 63) / 64))
     return GemmStatus::kBadAlignment;
   // MT=2's single accumulator serialises the epilogue with the next tile; on
@@ -1398,17 +1460,17 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   const int group_m = group_m_env != 0 ? group_m_env : (single ? 32 : 16 / pair_mt);
   if (out_f32) {
     e = pair_mt == 2 ? launch_pair<1, 1, 2, 1>(ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms,
-                                               group_m, epi, stream)
+                                               group_m, epi, stream, side)
                      : launch_pair<1, 1, 1, 1>(ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms,
-                                               group_m, epi, stream);
+                                               group_m, epi, stream, side);
   } else if (single) {
     e = op == 0 ? launch_single<0, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream)
         : op == 1 ? launch_single<0, 0>(ma, mb, C, ldc, m, n, k, num_sms, stream)
                   : launch_single<1, 1>(ma, mb, C, ldc, m, n, k, num_sms, stream);
   } else {
-    e = op == 0 ? launch_pair_mt<0, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream)
-        : op == 1 ? launch_pair_mt<0, 0>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream)
-                  : launch_pair_mt<1, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream);
+    e = op == 0 ? launch_pair_mt<0, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream, side)
+        : op == 1 ? launch_pair_mt<0, 0>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream, side)
+                  : launch_pair_mt<1, 1>(pair_mt, ma, mb, mc, use_tma_store, C, ldc, m, n, k, num_sms, group_m, epi, stream, side);
   }
   g_launch_error = e;
   return e == cudaSuccess ? GemmStatus::kOk : GemmStatus::kLaunch;

@@ -282,6 +282,11 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   int xsum2 = 0;
   if (const char* v = std::getenv("AXONN_XSUM")) xsum2 = std::atoi(v);
   if (flags & AXONN_LB_XSUM) xsum2 = 1;
+  // dÎ's 2-rank exchange summed inside the dW GEMM (SideSum), as on the
+  // multi-GPU path (AXONN_SIDESUM)
+  bool sidesum = false;
+  if (const char* v = std::getenv("AXONN_SIDESUM")) sidesum = std::atoi(v) != 0;
+  if (flags & AXONN_LB_SIDESUM) sidesum = true;
   const bool reverse = (flags & AXONN_LB_REVERSE) != 0;
   auto members = [&](int r, int axis) {
     std::vector<int> m(g[axis]);
@@ -395,6 +400,18 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
         if (!op->recv[r] || (op->P == 2 && !op->out[r]))
           return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
       }
+    }
+  }
+  // side sum of dÎ: per rank a parity counter and the go / finished words
+  // (no cross-rank barrier here: stream order already completed every rank's dI GEMM)
+  const bool side_on = sidesum && fi.mode == kExchange && fi.P == 2 && m_l > 0 && k_l > 0 &&
+                       n_l > 0 && fw.mode != kXSum;
+  std::vector<char*> side_ctrl(G, nullptr);
+  if (side_on) {
+    for (int r = 0; r < G; ++r) {
+      side_ctrl[r] = static_cast<char*>(pool.get(256));
+      if (!side_ctrl[r] || cudaMemsetAsync(side_ctrl[r], 0, 256, st) != cudaSuccess)
+        return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
     }
   }
   if (fz.mode == kScatter) {
@@ -632,14 +649,15 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
                      fi.mode == kStore ? nullptr : &t)) != AXONN_OK)
       return s;
   }
-  if ((s = owner_phase(fi)) != AXONN_OK) return s;
+  if (!side_on && (s = owner_phase(fi)) != AXONN_OK) return s;
   if (fi.mode != kStore) {
     p |= fi.mode == kMcRed ? AXONN_LB_PATH_BWD_RED
          : fi.mode == kPairSum ? AXONN_LB_PATH_BWD_PAIRSUM
          : fi.mode == kXSum ? AXONN_LB_PATH_BWD_XSUM
          : fi.mode == kExchange ? AXONN_LB_PATH_BWD_EXCHANGE : AXONN_LB_PATH_BWD_SCATTER;
-    for (int r = 0; r < G; ++r)
-      if ((s = deliver(fi, r, dI[r])) != AXONN_OK) return s;
+    if (!side_on)
+      for (int r = 0; r < G; ++r)
+        if ((s = deliver(fi, r, dI[r])) != AXONN_OK) return s;
   }
 
   // ------------------------------------------------ line 13: dW partial
@@ -658,9 +676,24 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       t = target(fw, r);
       tp = &t;
     }
+    SideSum side;
+    if (side_on) {  // rank r's dW GEMM sums rank r's exchange slots of dÎ
+      side.recv0 = fi.recv[r];
+      side.recv1 = fi.recv[r];
+      side.out = fi.out[r];
+      side.n16 = fi.elems * fi.es / 16;
+      side.par = reinterpret_cast<int*>(side_ctrl[r]);
+      side.go = reinterpret_cast<int*>(side_ctrl[r] + 64);
+      side.fin = reinterpret_cast<unsigned*>(side_ctrl[r] + 128);
+    }
     if ((s = rt_gemm(AXONN_OP_TN, d->dtype, k_l, n_l, m_l, I[r], k_l, dOa[r], n_l,
-                     tp ? nullptr : dW[r], n_l, st, tp)) != AXONN_OK)
+                     tp ? nullptr : dW[r], n_l, st, tp, side_on ? &side : nullptr)) != AXONN_OK)
       return s;
+  }
+  if (side_on) {
+    p |= AXONN_LB_PATH_BWD_SIDESUM;
+    for (int r = 0; r < G; ++r)
+      if ((s = deliver(fi, r, dI[r])) != AXONN_OK) return s;
   }
   // ------------------------------------------------ line 14: RS_z (Eq. 2)
   if (fz.mode == kScatter) {

@@ -15,7 +15,7 @@ namespace axonn {
 // (run_gemm in axonn.cpp): status + thread-local message on failure.
 axonn_status_t rt_gemm(int op, int dtype, int64_t M, int64_t N, int64_t K, const void* A,
                        int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                       cudaStream_t st, const EpiTarget* epi);
+                       cudaStream_t st, const EpiTarget* epi, const SideSum* side = nullptr);
 axonn_status_t rt_fail(axonn_status_t s, const char* msg);
 void rt_count_launch();
 int rt_num_sms();

@@ -269,12 +269,15 @@ def main():
         # (the default); "red": 2-rank axes reduce with multimem.red; "exchange": 2-rank axes
         # exchange whole partials and sum locally; "scatter": 2-rank axes use
         # the scatter + owner phase; "0": NCCL collectives (AXONN_FUSED=0)
-        for fused in ("xsum", "red", "exchange", "pairsum", "pairpull", "scatter", "0"):
+        for fused in ("xsum", "red", "exchange", "exchange_side", "pairsum", "pairpull", "scatter",
+                      "0"):
             os.environ["AXONN_FUSED"] = "0" if fused == "0" else "1"
             os.environ["AXONN_RED_MIN_K"] = "0" if fused == "red" else str(1 << 30)
             os.environ["AXONN_EXCHANGE"] = "0" if fused == "scatter" else "1"
             os.environ["AXONN_PAIRSUM"] = {"pairsum": "1", "pairpull": "2"}.get(fused, "0")
             os.environ["AXONN_XSUM"] = "1" if fused == "xsum" else "0"
+            # the backward's exchange of dÎ summed by the dW GEMM's helper warps, or by a pass
+            os.environ["AXONN_SIDESUM"] = "1" if fused == "exchange_side" else "0"
             ax.axonn_grid_init(*cfg)
             if fused == "red" and rank == 0:
                 print(f"cfg={cfg} fused status:",

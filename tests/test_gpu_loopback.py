@@ -160,6 +160,8 @@ def _expected_paths(cfg, transposed, flags, grad_f32=False):
         want.add(two("dp", not grad_f32))
     elif cfg[3] > 2:
         want.add("dp_scatter")
+    if "bwd_exchange" in want and (flags & 512):
+        want.add("bwd_sidesum")  # dÎ's exchange summed by the dW GEMM's helper warps
     return want
 
 
@@ -208,6 +210,7 @@ def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
     # exchange summed inside the GEMM (kXSum, opt-in: here the first rank of
     # each pair leaves its sums to the sweep, the second sums in the GEMM)
     check(ax, G, cfg, transposed, "int", 0)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_SIDESUM)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_XSUM)
