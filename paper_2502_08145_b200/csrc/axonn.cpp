@@ -630,6 +630,8 @@ axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0,
     g_launches.fetch_add(1);
     axonn::OwnerOut o;
     o.n_dst = 1;
+    o.local = 1;
+    o.fast = env_int("AXONN_SUM_FAST", 1);
     o.dst[0] = reinterpret_cast<unsigned long long>(f.out.ptr);
     if (act_z) {  // the GeLU rides on the local sum: Z to act_z, GELU(Z) to the output
       o.dst[0] = reinterpret_cast<unsigned long long>(act_z);

@@ -528,6 +528,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       for (int r = 0; r < G; ++r) {
         OwnerOut o;
         o.n_dst = 1;
+        o.local = 1;
         o.dst[0] = reinterpret_cast<unsigned long long>(op.out[r]);
         if (act_z) {
           o.dst[0] = reinterpret_cast<unsigned long long>((*act_z)[r]);

@@ -90,8 +90,34 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv0, const uint4* __r
   // parity counter past the value the producing GEMM read
   const uint4* __restrict__ recv = (par && ((*par - 1) & 1)) ? recv1 : recv0;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n16;
-       i += stride) {
+  long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (!F32 && P == 2 && out.fast && out.mode == kOwnPlain && out.n_dst == 1 && !out.act) {
+    // the 2-rank exchange's local sum (HBM-bound): 4 units per thread per
+    // step, 8 loads in flight; slot 0 + slot 1 in fp32, one RNE rounding
+    uint4* __restrict__ dst = reinterpret_cast<uint4*>(out.dst[0]);
+    for (; i0 + 3 * stride < n16; i0 += 4 * stride) {
+      uint4 a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = recv[i0 + u * stride];
+        b[u] = recv[n16 + i0 + u * stride];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t x[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, y[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(
+              (0.f + __uint_as_float(x[q] << 16)) + __uint_as_float(y[q] << 16),
+              (0.f + __uint_as_float(x[q] & 0xFFFF0000u)) + __uint_as_float(y[q] & 0xFFFF0000u));
+          o[q] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        dst[i0 + u * stride] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+  for (long long i = i0; i < n16; i += stride) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int src = 0; src < P; ++src) {
       const uint4 v = recv[src * n16 + i];
@@ -142,7 +168,7 @@ __global__ void k_owner_reduce(const uint4* __restrict__ recv0, const uint4* __r
       }
     }
   }
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (!out.local) asm volatile("fence.acq_rel.sys;" ::: "memory");  // remote writes performed
 }
 
 // AG_z pull on the SMs: dst[q*n16 + i] = src[q][i] for the P ranks' staged

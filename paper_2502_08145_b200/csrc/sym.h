@@ -67,6 +67,11 @@ struct OwnerOut {
   // itself still goes to dst[], e.g. Z saved for the backward; reading R18)
   int act = 0;
   unsigned long long act_dst = 0;
+  // every destination is this rank's own memory (the exchange's local sum):
+  // no system-scope fence at the end
+  int local = 0;
+  // 2-rank bf16 local sum: the 4-units-per-thread loop (AXONN_SUM_FAST=0: the generic one)
+  int fast = 1;
 };
 // Owner phase: sum the P slots of `slice` elements in `recv` (bf16, or fp32
 // when f32) in rank order 0..P-1 in fp32, round once (bf16), write per `out`.
