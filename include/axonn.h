@@ -280,6 +280,10 @@ enum {
   AXONN_LB_XSUM = 256,       /* 2-rank bf16 axes at every K: the exchange summed
                                 inside the GEMM (kXSum, AXONN_XSUM=1 on the
                                 multi-GPU path; opt-in, measured slower)      */
+  AXONN_LB_NO_REDPAIR = 1024, /* 2-rank bf16 axes below the multimem.red threshold:
+                                 not unicast red.add into both ranks' outputs
+                                 (kRedPair, the default there) but the exchange
+                                 + local sum (AXONN_REDPAIR=0)                 */
   AXONN_LB_SIDESUM = 512     /* the backward's 2-rank exchange of dÎ summed by the
                                 dW GEMM's helper warps instead of a separate
                                 pass (AXONN_SIDESUM=1 on the multi-GPU path;
@@ -299,7 +303,9 @@ enum {
   AXONN_LB_PATH_DP_PAIRSUM = 65536,
   AXONN_LB_PATH_FWD_XSUM = 131072, AXONN_LB_PATH_BWD_XSUM = 262144,
   AXONN_LB_PATH_DP_XSUM = 524288,
-  AXONN_LB_PATH_BWD_SIDESUM = 1048576  /* dÎ's exchange summed inside the dW GEMM */
+  AXONN_LB_PATH_BWD_SIDESUM = 1048576,  /* dÎ's exchange summed inside the dW GEMM */
+  AXONN_LB_PATH_FWD_REDPAIR = 2097152, AXONN_LB_PATH_BWD_REDPAIR = 4194304,
+  AXONN_LB_PATH_DP_REDPAIR = 8388608
 };
 axonn_status_t axonn_loopback_step(const axonn_fc_desc_t* desc, int gx, int gy, int gz, int gd,
                                    const void* const* I_local, const void* const* W_hat,

@@ -33,13 +33,14 @@ AXONN_ACT_NONE, AXONN_ACT_GELU = 0, 1
 AXIS = {"x": 0, "y": 1, "z": 2, "d": 3}
 AXONN_LB_RED_ALWAYS, AXONN_LB_RED_NEVER, AXONN_LB_GATHER_PULL, AXONN_LB_EMULATE_MC = 1, 2, 4, 8
 AXONN_LB_NO_EXCHANGE, AXONN_LB_PAIRSUM, AXONN_LB_REVERSE, AXONN_LB_PAIRPULL = 16, 32, 64, 128
-AXONN_LB_XSUM, AXONN_LB_SIDESUM = 256, 512
+AXONN_LB_XSUM, AXONN_LB_SIDESUM, AXONN_LB_NO_REDPAIR = 256, 512, 1024
 LB_PATHS = {"fwd_red": 1, "fwd_scatter": 2, "bwd_red": 4, "bwd_scatter": 8, "rs_z": 16,
             "dp_red": 32, "dp_scatter": 64, "dp_after_rs": 128, "gather_copy": 256,
             "gather_pull": 512, "multicast": 1024, "fwd_exchange": 2048, "bwd_exchange": 4096,
             "dp_exchange": 8192, "fwd_pairsum": 16384, "bwd_pairsum": 32768,
             "dp_pairsum": 65536, "fwd_xsum": 131072, "bwd_xsum": 262144, "dp_xsum": 524288,
-            "bwd_sidesum": 1048576}
+            "bwd_sidesum": 1048576, "fwd_redpair": 2097152, "bwd_redpair": 4194304,
+            "dp_redpair": 8388608}
 _STATUS_NAMES = {0: "OK", 1: "ARG", 2: "CONFIG", 3: "SHAPE", 4: "STATE", 5: "INFEASIBLE",
                  6: "CUDA", 7: "NCCL", 8: "UNSUPPORTED"}
 

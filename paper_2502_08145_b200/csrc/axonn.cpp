@@ -400,7 +400,7 @@ void fused_plan(axonn_fc::Fused* f, int axis, int64_t rows, int64_t cols, int64_
                                      env_int("AXONN_RED_MIN_K", 8192),
                                      env_int("AXONN_EXCHANGE", 1) != 0,
                                      env_int("AXONN_PAIRSUM", 0) != 0,
-                                     env_int("AXONN_XSUM", 0));
+                                     env_int("AXONN_XSUM", 0), env_int("AXONN_REDPAIR", 2));
   if (mode == axonn::kStore) return;
   f->elems = static_cast<size_t>(rows * cols);
   f->cols = cols;
@@ -439,6 +439,21 @@ bool fused_bind(axonn_fc::Fused* f, std::string* why) {
   if (f->epi.mode == axonn::kStore) return true;
   if (f->epi.mode == axonn::kMcRed) {
     f->epi = axonn::epi_red(reinterpret_cast<unsigned long long>(f->out.mc));
+    return true;
+  }
+  if (f->epi.mode == axonn::kRedPair) {
+    void* pout = axonn::sym_peer_ptr(&f->out, 1 - S.c[f->axis]);
+    if (!pout) {
+      *why = "peer address of the output window unavailable";
+      return false;
+    }
+    axonn::EpiTarget t;
+    t.mode = axonn::kRedPair;
+    t.P = 2;
+    t.me = S.c[f->axis];
+    t.mc = reinterpret_cast<unsigned long long>(f->out.ptr);
+    t.peer[0] = reinterpret_cast<unsigned long long>(pout);
+    f->epi = t;
     return true;
   }
   const int P = S.g[f->axis], me = S.c[f->axis];
@@ -593,7 +608,7 @@ axonn_status_t agree_all(bool* ok) {
 }
 
 axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
-  if (f.epi.mode == axonn::kMcRed) {
+  if (f.epi.mode == axonn::kMcRed || f.epi.mode == axonn::kRedPair) {
     // zero every rank's copy, and order that before any rank's reductions
     CUDA_TRY(cudaMemsetAsync(f.out.ptr, 0, f.elems * f.es, st));
     return fused_barrier(f.axis, st);

@@ -42,6 +42,11 @@ namespace axonn {
 //              and marks them done (peer[5] + 4u).  What is still open when
 //              the kernel ends is summed by sym_xsum_sweep, which also
 //              advances *par.  No barrier, no pass over the whole output.
+//   kRedPair   2-rank all-reduce by unicast reductions: each 16-B bf16 vector
+//              is red.add-ed into this rank's output (mc + offset) and into
+//              the peer's (peer[0] + offset, over NVLink); both outputs are
+//              zeroed (and a barrier passed) before the GEMM, so every element
+//              ends as RNE(a + b) on both ranks, bit-identical to NCCL.
 //   kRedLocal  red.global.add of each 16-B bf16 vector at mc + offset: the
 //              single-GPU loopback's stand-in for kMcRed when the device
 //              has no multicast support (axonn_loopback_step).
@@ -55,7 +60,7 @@ struct EpiTarget {
   const int* par = nullptr;
 };
 enum EpiMode { kStore = 0, kMcRed = 1, kScatter = 2, kRedLocal = 3, kExchange = 4, kPairSum = 5,
-               kXSum = 6 };
+               kXSum = 6, kRedPair = 7 };
 
 // A memory-bound task the GEMM's idle helper warps (2 and 3 of every CTA)
 // run beside its tiles: the local sum of a 2-rank exchange all-reduce whose

@@ -1043,6 +1043,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<MT, DEEP>::T
                 const uint64_t off =
                     static_cast<uint64_t>(static_cast<long long>(epi.me) * epi.slice + f) * ELEM;
                 for (int q = 0; q < epi.P; ++q) *reinterpret_cast<uint4*>(xbase[q] + off) = w;
+              } else if (epi.mode == kRedPair) {
+                const uint64_t off = (static_cast<uint64_t>(grow) * ldc + gcol) * 2;
+                ptx::red_add_bf16x8(epi.mc + off, w);
+                ptx::red_add_bf16x8_sys(epi.peer[0] + off, w);
               } else if (epi.mode == kRedLocal) {
                 ptx::red_add_bf16x8(epi.mc + (static_cast<uint64_t>(grow) * ldc + gcol) * 2, w);
               } else if (epi.mode == kScatter) {
@@ -1425,7 +1429,7 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
   if (epi.mode != kStore && (single || (N % unit) || (ldc % unit)))
     return GemmStatus::kBadAlignment;
   if (out_f32 && op != 2) return GemmStatus::kBadOp;  // fp32 output: the dW (TN) product only
-  if (out_f32 && (epi.mode == kMcRed || epi.mode == kRedLocal))
+  if (out_f32 && (epi.mode == kMcRed || epi.mode == kRedLocal || epi.mode == kRedPair))
     return GemmStatus::kBadAlignment;  // red.add is bf16 here
   if (epi.mode == kScatter && (ldc != N || epi.slice % unit || epi.P < 1 || epi.P > 8))
     return GemmStatus::kBadAlignment;

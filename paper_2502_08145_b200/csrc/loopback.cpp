@@ -282,6 +282,11 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   int xsum2 = 0;
   if (const char* v = std::getenv("AXONN_XSUM")) xsum2 = std::atoi(v);
   if (flags & AXONN_LB_XSUM) xsum2 = 1;
+  // unicast reductions into both ranks' outputs (kRedPair), as on the
+  // multi-GPU path (AXONN_REDPAIR)
+  int redpair2 = 2;
+  if (const char* v = std::getenv("AXONN_REDPAIR")) redpair2 = std::atoi(v);
+  if (flags & AXONN_LB_NO_REDPAIR) redpair2 = 0;
   // dÎ's 2-rank exchange summed inside the dW GEMM (SideSum), as on the
   // multi-GPU path (AXONN_SIDESUM)
   bool sidesum = false;
@@ -305,7 +310,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     op->es = es;
     op->elems = rows * cols;
     if (op->P == 1) return AXONN_OK;
-    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2, pairsum2, xsum2);
+    op->mode = fused_mode(op->P, es, rows, cols, kdim, red_min_k, exchange2, pairsum2, xsum2,
+                          redpair2);
     op->cols = cols;
     op->chunks = ((rows + 31) / 32) * ((cols + 63) / 64);
     if (op->mode == kStore) {
@@ -371,6 +377,12 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
         if (cudaMemsetAsync(op->ctrl[r], 0, pair_ctrl_bytes(op->chunks), st) != cudaSuccess)
           return rt_fail(AXONN_ERR_CUDA, "loopback: memset failed");
       }
+    }
+    if (op->mode == kRedPair) {  // each rank's output, zeroed before the GEMMs
+      op->out.resize(G);
+      for (int r = 0; r < G; ++r)
+        if (!(op->out[r] = static_cast<char*>(pool.get(op->elems * op->es))))
+          return rt_fail(AXONN_ERR_CUDA, "loopback: cudaMalloc failed");
     }
     if (op->mode == kXSum) {  // two receive sets of 2 slots, output, control block
       const long long U = xsum_units(op->elems / op->cols, op->cols);
@@ -457,6 +469,16 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
       t.peer[5] = reinterpret_cast<unsigned long long>(op.ctrl[peer] + done);
       return t;
     }
+    if (op.mode == kRedPair) {  // as fused_bind in axonn.cpp
+      const std::vector<int> mem = members(r, op.axis);
+      EpiTarget t;
+      t.mode = kRedPair;
+      t.P = 2;
+      t.me = cc[r][op.axis];
+      t.mc = reinterpret_cast<unsigned long long>(op.out[r]);
+      t.peer[0] = reinterpret_cast<unsigned long long>(op.out[mem[1 - t.me]]);
+      return t;
+    }
     if (op.mode == kXSum) {  // as fused_bind in axonn.cpp
       const std::vector<int> mem = members(r, op.axis);
       const int me = cc[r][op.axis];
@@ -497,6 +519,12 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     return o;
   };
   auto zero_regions = [&](const LbOp& op) -> axonn_status_t {
+    if (op.mode == kRedPair) {
+      for (int r = 0; r < G; ++r)
+        if (cudaMemsetAsync(op.out[r], 0, op.elems * op.es, st) != cudaSuccess)
+          return rt_fail(AXONN_ERR_CUDA, "loopback: memset failed");
+      return AXONN_OK;
+    }
     if (op.mode != kMcRed) return AXONN_OK;
     for (const auto& kv : op.region)
       if (cudaMemsetAsync(arena.uc + kv.second, 0, op.elems * op.es, st) != cudaSuccess)
@@ -554,7 +582,8 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
   // the reduced result of rank r -> its caller buffer
   auto deliver = [&](const LbOp& op, int r, void* dst) -> axonn_status_t {
     const char* src =
-        ((op.mode == kScatter || op.mode == kExchange || op.mode == kPairSum || op.mode == kXSum) &&
+        ((op.mode == kScatter || op.mode == kExchange || op.mode == kPairSum || op.mode == kXSum ||
+          op.mode == kRedPair) &&
          op.P == 2)
             ? op.out[r]
             : uc_of(op, r);
@@ -618,6 +647,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     p |= fo.mode == kMcRed ? AXONN_LB_PATH_FWD_RED
          : fo.mode == kPairSum ? AXONN_LB_PATH_FWD_PAIRSUM
          : fo.mode == kXSum ? AXONN_LB_PATH_FWD_XSUM
+         : fo.mode == kRedPair ? AXONN_LB_PATH_FWD_REDPAIR
          : fo.mode == kExchange ? AXONN_LB_PATH_FWD_EXCHANGE : AXONN_LB_PATH_FWD_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fo, r, O[r])) != AXONN_OK) return s;
@@ -655,6 +685,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     p |= fi.mode == kMcRed ? AXONN_LB_PATH_BWD_RED
          : fi.mode == kPairSum ? AXONN_LB_PATH_BWD_PAIRSUM
          : fi.mode == kXSum ? AXONN_LB_PATH_BWD_XSUM
+         : fi.mode == kRedPair ? AXONN_LB_PATH_BWD_REDPAIR
          : fi.mode == kExchange ? AXONN_LB_PATH_BWD_EXCHANGE : AXONN_LB_PATH_BWD_SCATTER;
     if (!side_on)
       for (int r = 0; r < G; ++r)
@@ -722,6 +753,7 @@ axonn_status_t loopback_step(const axonn_fc_desc_t* d, const int g[4], const voi
     p |= fw.mode == kMcRed ? AXONN_LB_PATH_DP_RED
          : fw.mode == kPairSum ? AXONN_LB_PATH_DP_PAIRSUM
          : fw.mode == kXSum ? AXONN_LB_PATH_DP_XSUM
+         : fw.mode == kRedPair ? AXONN_LB_PATH_DP_REDPAIR
          : fw.mode == kExchange ? AXONN_LB_PATH_DP_EXCHANGE : AXONN_LB_PATH_DP_SCATTER;
     for (int r = 0; r < G; ++r)
       if ((s = deliver(fw, r, dW[r])) != AXONN_OK) return s;

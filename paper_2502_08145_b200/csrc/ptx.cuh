@@ -308,6 +308,12 @@ __device__ __forceinline__ void red_add_bf16x8(uint64_t addr, uint4 v) {
                "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
+// bf16x8 add-reduction into an NVLink peer's memory (kRedPair)
+__device__ __forceinline__ void red_add_bf16x8_sys(uint64_t addr, uint4 v) {
+  asm volatile("red.relaxed.sys.global.add.noftz.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(addr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 // System-scope atomics on local or NVLink-peer (LSA) addresses (kPairSum).

@@ -473,7 +473,7 @@ cudaError_t sym_gather_copy(const void* const* src, int P, size_t bytes, void* d
 }
 
 int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
-               bool exchange2, bool pairsum2, int xsum2) {
+               bool exchange2, bool pairsum2, int xsum2, int redpair2) {
   const int64_t n = rows * cols;
   const int unit = 16 / es;  // elements per 16-B epilogue unit
   // not fused: a 1-rank axis, an empty output, rows not a whole number of
@@ -483,6 +483,8 @@ int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_
   if (es == 2 && P == 2 && pairsum2) return kPairSum;
   // 2-rank bf16: exchange, summed inside the GEMM as partials land
   if (es == 2 && P == 2 && (xsum2 == 1 || (xsum2 == 2 && kdim < red_min_k))) return kXSum;
+  // 2-rank bf16: unicast reductions into both ranks' outputs
+  if (es == 2 && P == 2 && (redpair2 == 1 || (redpair2 == 2 && kdim < red_min_k))) return kRedPair;
   // multimem.red.add sums bf16 here; fp32 always takes the scatter + owner phase
   if (es == 2 && P == 2 && kdim >= red_min_k) return kMcRed;
   // 2-rank axes: exchange whole partials, then sum locally (no owner broadcast)

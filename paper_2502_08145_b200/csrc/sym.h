@@ -103,8 +103,10 @@ cudaError_t sym_barrier(SymAxis* a, cudaStream_t st, int index = 0, int* ctr = n
 // (exchange2) the exchange of whole partials, else the scatter + owner phase.
 // xsum2: 1 = 2-rank bf16 axes sum inside the GEMM (kXSum) at every K;
 // 2 = only below red_min_k (multimem.red above); 0 = never.
+// redpair2: 1 = 2-rank bf16 axes reduce by unicast red.add into both ranks'
+// outputs (kRedPair) at every K; 2 = only below red_min_k; 0 = never.
 int fused_mode(int P, int es, int64_t rows, int64_t cols, int64_t kdim, int red_min_k,
-               bool exchange2, bool pairsum2, int xsum2 = 0);
+               bool exchange2, bool pairsum2, int xsum2 = 0, int redpair2 = 0);
 // kXSum: the control block (per rank, symmetric): [0, 4U) the flags the peer
 // raises per 32x128 output unit, [4U, 8U) this rank's done marks, then the
 // call counter (the parity of the receive set, the flag epoch) and the

@@ -269,13 +269,15 @@ def main():
         # (the default); "red": 2-rank axes reduce with multimem.red; "exchange": 2-rank axes
         # exchange whole partials and sum locally; "scatter": 2-rank axes use
         # the scatter + owner phase; "0": NCCL collectives (AXONN_FUSED=0)
-        for fused in ("xsum", "red", "exchange", "exchange_side", "pairsum", "pairpull", "scatter",
-                      "0"):
+        for fused in ("xsum", "red", "redpair", "exchange", "exchange_side", "pairsum", "pairpull",
+                      "scatter", "0"):
             os.environ["AXONN_FUSED"] = "0" if fused == "0" else "1"
             os.environ["AXONN_RED_MIN_K"] = "0" if fused == "red" else str(1 << 30)
             os.environ["AXONN_EXCHANGE"] = "0" if fused == "scatter" else "1"
             os.environ["AXONN_PAIRSUM"] = {"pairsum": "1", "pairpull": "2"}.get(fused, "0")
             os.environ["AXONN_XSUM"] = "1" if fused == "xsum" else "0"
+            # "redpair": unicast red.add at every K (the default uses it below the red threshold)
+            os.environ["AXONN_REDPAIR"] = "1" if fused == "redpair" else "0"
             # the backward's exchange of dÎ summed by the dW GEMM's helper warps, or by a pass
             os.environ["AXONN_SIDESUM"] = "1" if fused == "exchange_side" else "0"
             ax.axonn_grid_init(*cfg)
@@ -302,7 +304,7 @@ def main():
                             for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
                                 assert np.array_equal(a, b), f"zero-copy differs {cfg}"
             run_chain(cfg, "uniform", torch.bfloat16, rank)
-            if fused in ("xsum", "red", "exchange", "pairsum", "pairpull", "0"):
+            if fused in ("xsum", "red", "redpair", "exchange", "pairsum", "pairpull", "0"):
                 run_graph(cfg, rank)
                 run_empty(cfg, rank)
             if fused == "0":

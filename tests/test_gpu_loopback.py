@@ -145,6 +145,8 @@ def _expected_paths(cfg, transposed, flags, grad_f32=False):
             return f"{name}_pairsum"
         if xs and es2:
             return f"{name}_xsum"
+        if es2 and not red2 and not (flags & 1024):
+            return f"{name}_redpair"  # the default below the multimem.red threshold
         return f"{name}_red" if (red2 and es2) else (f"{name}_scatter" if no_x else f"{name}_exchange")
     for name, P in (("fwd", cfg[ax_f]), ("bwd", cfg[ax_b])):
         if P == 2:
@@ -204,15 +206,19 @@ CASES = [(G, cfg) for G in (2, 3, 4, 6, 8) for cfg in grid.enumerate_configs(G)]
 @pytest.mark.parametrize("transposed", [False, True])
 @pytest.mark.parametrize("G,cfg", CASES, ids=[f"{c[0]}{c[1]}{c[2]}{c[3]}" for _, c in CASES])
 def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
-    # default 2-rank mode for these short K (exchange of whole partials) and
-    # the copy-engine AG_z; multimem.red forced on 2-rank axes with the
-    # SM-pull AG_z; the 2-rank scatter + owner phase (exchange off); the
-    # exchange summed inside the GEMM (kXSum, opt-in: here the first rank of
-    # each pair leaves its sums to the sweep, the second sums in the GEMM)
+    # default 2-rank mode for these short K (unicast red.add into both ranks'
+    # outputs, kRedPair) and the copy-engine AG_z; the exchange of whole
+    # partials + local sum, and with the dW GEMM doing that sum (SideSum);
+    # multimem.red forced on 2-rank axes with the SM-pull AG_z; the 2-rank
+    # scatter + owner phase; the exchange summed inside the GEMM (kXSum,
+    # opt-in: here the first rank of each pair leaves its sums to the sweep,
+    # the second sums in the GEMM)
+    nr = ax.AXONN_LB_NO_REDPAIR
     check(ax, G, cfg, transposed, "int", 0)
-    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_SIDESUM)
+    check(ax, G, cfg, transposed, "int", nr)
+    check(ax, G, cfg, transposed, "int", nr | ax.AXONN_LB_SIDESUM)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_RED_ALWAYS | ax.AXONN_LB_GATHER_PULL)
-    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE)
+    check(ax, G, cfg, transposed, "int", nr | ax.AXONN_LB_NO_EXCHANGE)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_XSUM)
     check(ax, G, cfg, transposed, "int", ax.AXONN_LB_XSUM | ax.AXONN_LB_REVERSE)
     # the sum finished inside the epilogue (kPairSum), each rank of a pair in
@@ -231,6 +237,7 @@ def test_every_grid_integer_bit_exact(ax, G, cfg, transposed):
 def test_every_grid_uniform_within_tolerance(ax, G, cfg, transposed):
     check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_RED_ALWAYS)
     check(ax, G, cfg, transposed, "uniform", ax.AXONN_LB_XSUM)
+    check(ax, G, cfg, transposed, "uniform", 0)
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 2, 1), (1, 1, 1, 2), (1, 1, 4, 2), (1, 1, 2, 4),
@@ -240,7 +247,8 @@ def test_fp32_gradients_bit_exact(ax, cfg, transposed):
     """AXONN_BF16_GRADF32 (R17): fp32 dW epilogue, fp32 RS_z / DP owner phases."""
     G = int(np.prod(cfg))
     check(ax, G, cfg, transposed, "int", 0, grad_f32=True)
-    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE, grad_f32=True)
+    check(ax, G, cfg, transposed, "int", ax.AXONN_LB_NO_EXCHANGE | ax.AXONN_LB_NO_REDPAIR,
+          grad_f32=True)
     check(ax, G, cfg, transposed, "uniform", 0, grad_f32=True)
 
 
@@ -301,7 +309,7 @@ FULL = [  # (name, h, m, grid, layers): tensor-parallel proxies of BASELINE C3/C
 ]
 
 
-@pytest.mark.parametrize("flags", [0, 256], ids=["red_exchange", "xsum"])
+@pytest.mark.parametrize("flags", [0, 256, 1024], ids=["default", "xsum", "exchange"])
 @pytest.mark.parametrize("name,h,m,cfg,which", FULL, ids=[f[0] for f in FULL])
 def test_full_size_tensor_parallel(ax, name, h, m, cfg, which, flags):
     """Full-size GPT-block layers on tensor-parallel grids, every rank on this
@@ -408,9 +416,10 @@ def test_gelu_layer(ax, cfg, transposed):
     elementwise pass after the other forward modes; dGeLU before line 11."""
     G = int(np.prod(cfg))
     paths = check_act(ax, G, cfg, transposed, 0)
+    paths_e = check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_REDPAIR)
     paths_x = check_act(ax, G, cfg, transposed, ax.AXONN_LB_XSUM)
     check_act(ax, G, cfg, transposed, ax.AXONN_LB_RED_ALWAYS)
-    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE)
+    check_act(ax, G, cfg, transposed, ax.AXONN_LB_NO_EXCHANGE | ax.AXONN_LB_NO_REDPAIR)
     ax_f = 0 if transposed else 1
     if cfg[ax_f] == 2:
-        assert "fwd_exchange" in paths and "fwd_xsum" in paths_x
+        assert "fwd_redpair" in paths and "fwd_exchange" in paths_e and "fwd_xsum" in paths_x
