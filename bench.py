@@ -694,13 +694,20 @@ def run_config(c, spec, steps, warmup, e2e_on, exposure_on):
             scratch.append((g, torch.empty(g.k_l, g.n_l, dtype=bf, device="cuda").uniform_(-a, a),
                             torch.empty(g.k_l, g.n_l, dtype=gdt, device="cuda")))
 
+        # the GEMM-only reference writes its forward outputs to scratch: the
+        # handle-owned output buffers are read-only for the caller
+        # (include/axonn.h, axonn_fc_output_buffer)
+        Oscr = [torch.empty(l["g"].m_l, l["g"].n_l, dtype=bf, device="cuda") for l in L]
+        dIscr = [torch.empty(l["g"].m_l, l["g"].k_l, dtype=bf, device="cuda") for l in L]
+
         def gemm_step(s):
-            for l, (g, Wf, _) in zip(L, scratch):
-                ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, s)
-            for l, (g, Wf, dWf) in zip(reversed(L), reversed(scratch)):
+            for l, (g, Wf, _), Os in zip(L, scratch, Oscr):
+                ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, Os, g.n_l, s)
+            for l, (g, Wf, dWf), Os, dIs in zip(reversed(L), reversed(scratch), reversed(Oscr),
+                                                 reversed(dIscr)):
                 if args.recompute:
-                    ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, s)
-                ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, s)
+                    ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, Os, g.n_l, s)
+                ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, dIs, g.k_l, s)
                 ax.axonn_gemm(2, gcode, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, s)
 
         for _ in range(2):
@@ -743,10 +750,10 @@ def run_config(c, spec, steps, warmup, e2e_on, exposure_on):
                 ev["sync"][2 * rep + 1].record(stream)
                 for i, (l, (g, Wf, dWf)) in enumerate(zip(L, scratch)):
                     ev[f"{names[i]}_fwd_gemm"][2 * rep].record(stream)
-                    ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, l["O"], g.n_l, stream)
+                    ax.axonn_gemm(0, 0, g.m_l, g.n_l, g.k_l, l["I"], g.k_l, Wf, g.n_l, Oscr[i], g.n_l, stream)
                     ev[f"{names[i]}_fwd_gemm"][2 * rep + 1].record(stream)
                     ev[f"{names[i]}_bwd_gemm"][2 * rep].record(stream)
-                    ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, l["dI"], g.k_l, stream)
+                    ax.axonn_gemm(1, 0, g.m_l, g.k_l, g.n_l, l["dO"], g.n_l, Wf, g.n_l, dIscr[i], g.k_l, stream)
                     ax.axonn_gemm(2, gcode, g.k_l, g.n_l, g.m_l, l["I"], g.k_l, l["dO"], g.n_l, dWf, g.n_l, stream)
                     ev[f"{names[i]}_bwd_gemm"][2 * rep + 1].record(stream)
         barrier()

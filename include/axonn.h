@@ -163,7 +163,11 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
  * not a multiple of 8, or AXONN_FUSED=0).  Passing the returned pointer as the
  * output argument of axonn_fc_forward / axonn_fc_backward avoids the final
  * device-to-device copy; its contents are valid until the next call that
- * writes that output.  Errors: ARG. */
+ * writes that output.  The buffer is read-only for the caller: when it is
+ * passed on as another layer's I_local (dO_local), the library may zero it
+ * in the background once that layer's backward, its last reader, has been
+ * enqueued (the 2-rank red.add reduction's next use needs it zeroed).
+ * Errors: ARG. */
 axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr);
 /* "fused" if collectives along `axis` (0=X,1=Y,2=Z,3=DATA) of the current grid
  * are fused into the GEMM epilogue over NVLS, else the reason (host buf). */

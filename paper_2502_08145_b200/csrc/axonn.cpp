@@ -100,6 +100,11 @@ struct State {
   int64_t comm_bytes[5] = {0, 0, 0, 0, 0};  // ring bytes sent per rank: ag_z, rs_z, ar_fwd, ar_bwd, ar_d
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_free;
+  // background zeroing of kRedPair outputs (copy engines): a stream and a
+  // zero source the copies read from
+  cudaStream_t zstream = nullptr;
+  void* zsrc = nullptr;
+  size_t zsrc_bytes = 0;
 };
 
 State S;
@@ -340,6 +345,10 @@ struct axonn_fc {
     axonn::SymBuf ctrl;   // pair-sum mode: arbitration tickets + done / call counters;
                           // exchange mode: the side-sum words (arrive, go, finished)
     int* side_arrive_peer = nullptr;  // exchange mode: the peer's arrive word (LSA)
+    // kRedPair: the output was zeroed in the background once its last reader
+    // (the next layer's backward) was enqueued; the next use waits for it
+    bool prezeroed = false;
+    cudaEvent_t ev_zeroed = nullptr;
     long long chunks = 0; // pair-sum mode: 32 x 64 output chunks
     int64_t cols = 0;     // row length of the reduced output
     axonn::EpiTarget epi;
@@ -590,6 +599,9 @@ void fused_reset(axonn_fc::Fused* f) {
   f->epi = axonn::EpiTarget();
   f->out_peer = nullptr;
   f->side_arrive_peer = nullptr;
+  if (f->ev_zeroed) cudaEventDestroy(f->ev_zeroed);
+  f->ev_zeroed = nullptr;
+  f->prezeroed = false;
   f->elems = 0;
 }
 
@@ -608,12 +620,56 @@ axonn_status_t agree_all(bool* ok) {
 }
 
 axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
+  if (f.epi.mode == axonn::kRedPair && f.prezeroed) {
+    // zeroed on the copy engines after its last reader; every rank's zeroing
+    // is ordered before its barrier, so after it every copy is zero
+    f.prezeroed = false;
+    CUDA_TRY(cudaStreamWaitEvent(st, f.ev_zeroed, 0));
+    return fused_barrier(f.axis, st);
+  }
   if (f.epi.mode == axonn::kMcRed || f.epi.mode == axonn::kRedPair) {
     // zero every rank's copy, and order that before any rank's reductions
     CUDA_TRY(cudaMemsetAsync(f.out.ptr, 0, f.elems * f.es, st));
     return fused_barrier(f.axis, st);
   }
   return AXONN_OK;  // scatter: the previous use's final barrier already freed the slots
+}
+
+// `buf` (a layer input or output gradient the caller passed) is read for the
+// last time by work already enqueued on `st`.  If it is a kRedPair output of
+// some layer, zero it now on the copy engines, off the critical path; its
+// next fused_pre then only waits for that (AXONN_PREZERO=0: zero inline).
+axonn_status_t prezero_after(const void* buf, cudaStream_t st) {
+  static const bool on = env_int("AXONN_PREZERO", 1) != 0;
+  if (!on || !buf) return AXONN_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return AXONN_OK;  // graphs: zero inline at the next use
+  for (axonn_fc* o : S.handles) {
+    for (axonn_fc::Fused* f : {&o->fo, &o->fi}) {
+      if (f->epi.mode != axonn::kRedPair || f->out.ptr != buf || f->prezeroed) continue;
+      const size_t bytes = f->elems * f->es;
+      if (!S.zstream)
+        CUDA_TRY(cudaStreamCreateWithFlags(&S.zstream, cudaStreamNonBlocking));
+      if (S.zsrc_bytes < (size_t(32) << 20)) {
+        if (S.zsrc) CUDA_TRY(cudaFree(S.zsrc));
+        S.zsrc_bytes = size_t(32) << 20;
+        CUDA_TRY(cudaMalloc(&S.zsrc, S.zsrc_bytes));
+        CUDA_TRY(cudaMemset(S.zsrc, 0, S.zsrc_bytes));
+        CUDA_TRY(cudaDeviceSynchronize());
+      }
+      if (!f->ev_zeroed) CUDA_TRY(cudaEventCreateWithFlags(&f->ev_zeroed, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(f->ev_zeroed, st));
+      CUDA_TRY(cudaStreamWaitEvent(S.zstream, f->ev_zeroed, 0));
+      for (size_t o2 = 0; o2 < bytes; o2 += S.zsrc_bytes)
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(f->out.ptr) + o2, S.zsrc,
+                                 std::min(S.zsrc_bytes, bytes - o2), cudaMemcpyDeviceToDevice,
+                                 S.zstream));
+      CUDA_TRY(cudaEventRecord(f->ev_zeroed, S.zstream));
+      f->prezeroed = true;
+    }
+  }
+  return AXONN_OK;
 }
 
 axonn_status_t fused_post(axonn_fc::Fused& f, cudaStream_t st, int index = 0,
@@ -887,6 +943,11 @@ axonn_status_t axonn_grid_finalize(void) {
   S.pending_grads.clear();
   if (S.flag_dev) cudaFree(S.flag_dev);
   S.flag_dev = nullptr;
+  if (S.zstream) cudaStreamDestroy(S.zstream);
+  if (S.zsrc) cudaFree(S.zsrc);
+  S.zstream = nullptr;
+  S.zsrc = nullptr;
+  S.zsrc_bytes = 0;
   S.grid = false;
   return AXONN_OK;
 }
@@ -1161,6 +1222,7 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
     return fail(AXONN_ERR_ARG, "NULL tensor");
   STATUS_TRY(check_async_nccl());
   cudaStream_t st = as_stream(stream);
+  const void* dO_caller = dO_local;  // another layer's output buffer, possibly
   if (h->zbuf && g.m_l != 0 && g.n_l != 0) {
     // dZ = dO ⊙ GELU'(Z) replaces dO in lines 11 and 13 (R18)
     CUDA_TRY(axonn::gelu_backward(dO_local, h->zbuf, h->dzbuf, g.m_l * g.n_l, S.num_sms, st));
@@ -1338,6 +1400,10 @@ axonn_status_t axonn_fc_backward(axonn_fc_t h, const void* dO_local, void* dI_lo
   }
   // dI must be complete in `stream` order when we return
   if (Pb > 1 && !fI) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_ar, 0));
+  // this backward was the last reader of its cached input and of dO: if
+  // either is another layer's red.add output, zero it in the background
+  STATUS_TRY(prezero_after(h->I, st));
+  STATUS_TRY(prezero_after(dO_caller, st));
   h->have_fwd = false;
   return AXONN_OK;
 }

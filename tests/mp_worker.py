@@ -191,6 +191,64 @@ def run_chain(cfg, kind, dtype, rank):
         print(f"ok chain N->T cfg={cfg} {kind}/{dtype}", flush=True)
 
 
+def run_chain_zero_copy(cfg, rank, steps=3):
+    """The chained pair of run_chain through the handle-owned output buffers
+    (layer 2's I_local IS layer 1's output buffer, layer 1's dO_local IS layer
+    2's dI buffer), for several steps: a reduction buffer that the library
+    zeroes in the background after its last reader (2-rank red.add outputs)
+    must give every step the same bits, within tolerance of the oracle."""
+    from bench import copy_raw
+    m, k, hdim, n = 256, 128, 256, 128
+    X = synthdata.tensor((m, k), 311)
+    W1 = synthdata.tensor((k, hdim), 312)
+    W2 = synthdata.tensor((hdim, n), 313)
+    dY = synthdata.tensor((m, n), 314)
+    bf = torch.bfloat16
+    h1 = ax.axonn_fc_create(m, k, hdim, False, ax.AXONN_BF16)
+    h2 = ax.axonn_fc_create(m, hdim, n, True, ax.AXONN_BF16)
+    g1, g2 = ax.axonn_fc_geometry(h1), ax.axonn_fc_geometry(h2)
+
+    def what(W, g):
+        Wl = np.ascontiguousarray(W[g.in_col0:g.in_col0 + g.k_l, g.out_col0:g.out_col0 + g.n_l])
+        return dev(Wl.reshape(1, -1)[:, g.what_off:g.what_off + g.what_len], bf).reshape(-1)
+
+    I1 = dev(X[g1.row0:g1.row0 + g1.m_l, g1.in_col0:g1.in_col0 + g1.k_l], bf)
+    dO2 = dev(dY[g2.row0:g2.row0 + g2.m_l, g2.out_col0:g2.out_col0 + g2.n_l], bf)
+    Wh1, Wh2 = what(W1, g1), what(W2, g2)
+    O1 = ax.axonn_fc_output_buffer(h1, 0) or torch.empty((g1.m_l, g1.n_l), dtype=bf, device="cuda")
+    dI2 = ax.axonn_fc_output_buffer(h2, 1) or torch.empty((g2.m_l, g2.k_l), dtype=bf, device="cuda")
+    O2 = torch.empty((g2.m_l, g2.n_l), dtype=bf, device="cuda")
+    dI1 = torch.empty((g1.m_l, g1.k_l), dtype=bf, device="cuda")
+    dW1 = torch.empty((g1.what_len,), dtype=bf, device="cuda")
+    dW2 = torch.empty((g2.what_len,), dtype=bf, device="cuda")
+    s = torch.cuda.current_stream()
+    outs = []
+    for _ in range(steps):
+        ax.axonn_fc_forward(h1, I1, Wh1, O1, s)
+        ax.axonn_fc_forward(h2, O1, Wh2, O2, s)
+        ax.axonn_fc_backward(h2, dO2, dI2, dW2, s)
+        ax.axonn_fc_backward(h1, dI2, dI1, dW1, s)
+        ax.axonn_grads_sync(s)
+        O1c = torch.empty((g1.m_l, g1.n_l), dtype=bf, device="cuda")
+        copy_raw(O1c.data_ptr(), O1 if isinstance(O1, int) else O1.data_ptr(), 2 * O1c.numel(), s)
+        torch.cuda.synchronize()
+        outs.append([host(t) for t in (O1c, O2, dI1, dW1, dW2)])
+    ax.axonn_fc_destroy(h1)
+    ax.axonn_fc_destroy(h2)
+    for st in outs[1:]:
+        for name, a, b in zip(("O1", "O2", "dX", "dW1", "dW2"), outs[0], st):
+            assert np.array_equal(a, b), f"zero-copy chain: step differs in {name} cfg={cfg} rank {rank}"
+    rO1 = fc.fc_forward(X, W1)
+    rO2 = fc.fc_forward(rO1, W2)
+    rdX = fc.fc_backward_input(fc.fc_backward_input(dY, W2), W1)
+    for name, got, ref in (("O2", outs[0][1], rO2[g2.row0:g2.row0 + g2.m_l, g2.out_col0:g2.out_col0 + g2.n_l]),
+                           ("dX", outs[0][2], rdX[g1.row0:g1.row0 + g1.m_l, g1.in_col0:g1.in_col0 + g1.k_l])):
+        err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
+        assert err <= 2e-2, f"zero-copy chain {name} normwise {err} cfg={cfg} rank {rank}"
+    if rank == 0:
+        print(f"ok zero-copy chain x{steps} cfg={cfg}", flush=True)
+
+
 def run_graph(cfg, rank):
     """One layer step (OAG prefetch, forward, backward, grads_sync) captured in a
     CUDA graph — NCCL calls, device-side barriers, copy-engine gathers and the
@@ -304,6 +362,8 @@ def main():
                             for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
                                 assert np.array_equal(a, b), f"zero-copy differs {cfg}"
             run_chain(cfg, "uniform", torch.bfloat16, rank)
+            if fused in ("exchange", "redpair"):
+                run_chain_zero_copy(cfg, rank)
             if fused in ("xsum", "red", "redpair", "exchange", "pairsum", "pairpull", "0"):
                 run_graph(cfg, rank)
                 run_empty(cfg, rank)
