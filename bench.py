@@ -11,9 +11,14 @@ PAPER.md:402-414), then their backward in reverse order, then the ORS /
 data-parallel wait point (axonn_grads_sync).
 
 N = 1: BASELINE.json configs[1] (C2): GPT-5B block, m = 16,384 tokens, grid
-1x1x1x1.  N > 1: the same block weak-scaled (16,384 tokens per GPU, global
-m = 16,384 N) on the grid the paper's performance model ranks first
-(axonn_grid_select, uniform NVSwitch bandwidth), unless --grid is given.
+1x1x1x1.  N > 1 measures the 3D PMM on tensor grids (PRIMARY below): N = 8
+is C3 exactly (GPT-20B block, m = 16,384, grid 2x2x2x1); N = 4 the C3 proxy
+(m = 8192 on 2x2x1x1: C3's local GEMMs and all-reduce sizes); N = 2 the
+20B block on 2x1x1x1 at C3's per-GPU flops.  Sub-records of the same line
+(SUB): the C4a / C4b (80B, phase B) and C5 (40B, tensor x data) configs or
+their 4-GPU proxies, and the data-parallel weak-scaling line (5B, 16,384
+tokens per GPU, the grid the paper's performance model ranks first with the
+measured Case-1 table).  --grid / --model / --tokens override the plan.
 
 value = model flops of the step (6 m k n per layer, PAPER.md:786-795,
 SPEC.md:443) summed over ranks / device time of the step (CUDA events on the
