@@ -166,7 +166,8 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
  * writes that output.  The buffer is read-only for the caller: when it is
  * passed on as another layer's I_local (dO_local), the library may zero it
  * in the background once that layer's backward, its last reader, has been
- * enqueued (the 2-rank red.add reduction's next use needs it zeroed).
+ * enqueued (the 2-rank red.add reduction's next use needs it zeroed).  A
+ * buffer that feeds more than one layer needs AXONN_PREZERO=0.
  * Errors: ARG. */
 axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr);
 /* "fused" if collectives along `axis` (0=X,1=Y,2=Z,3=DATA) of the current grid
