@@ -177,7 +177,8 @@ axonn_status_t axonn_fused_status(int axis, char* buf, int cap);
 /* Diagnostics: bytes/s one rank moves over NVLink with one primitive on the
  * symmetric memory of `axis` (mode 0: multimem.red.add bf16, 1: multimem.st,
  * 2: plain 16-B stores to the next rank's copy, 3: multimem.ld_reduce,
- * 4: local stores), `ctas` x 512 threads.  Collective over the axis. */
+ * 4: local stores, 5: red.add bf16 into the next rank's copy, 6: local
+ * red.add bf16), `ctas` x 512 threads.  Collective over the axis. */
 axonn_status_t axonn_nvlink_probe(int axis, int64_t bytes, int mode, int ctas, int iters,
                                   double* gbps);
 

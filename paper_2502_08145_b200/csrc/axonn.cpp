@@ -1102,7 +1102,7 @@ axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr) {
 axonn_status_t axonn_nvlink_probe(int axis, int64_t bytes, int mode, int ctas, int iters,
                                   double* gbps) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
-  if (axis < 0 || axis > 3 || bytes <= 0 || mode < 0 || mode > 4 || ctas < 1 || iters < 1 || !gbps)
+  if (axis < 0 || axis > 3 || bytes <= 0 || mode < 0 || mode > 6 || ctas < 1 || iters < 1 || !gbps)
     return fail(AXONN_ERR_ARG, "bad argument");
   if (!S.sym[axis].impl) return fail(AXONN_ERR_STATE, "axis %d has no symmetric memory: %s", axis,
                                      S.sym_why[axis].c_str());

@@ -60,6 +60,13 @@ __global__ void k_probe(uint4* local, uint64_t target, size_t n16, int mode) {
                    "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
     } else if (mode == 2) {
       *reinterpret_cast<uint4*>(a) = v;               // plain store to a peer (LSA) address
+    } else if (mode == 5) {                           // unicast red.add into a peer (kRedPair)
+      asm volatile("red.relaxed.sys.global.add.noftz.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(a),
+                   "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    } else if (mode == 6) {                           // local red.add (kRedPair's own output)
+      asm volatile("red.relaxed.gpu.global.add.noftz.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(
+                       reinterpret_cast<uint64_t>(local + i)),
+                   "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
     } else if (mode == 3) {
       uint32_t x0, x1, x2, x3;
       asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
@@ -425,7 +432,7 @@ void* sym_peer_ptr(SymBuf* b, int peer) {
 
 cudaError_t sym_probe(SymAxis* a, SymBuf* b, int mode, int peer, int ctas, int iters, float* ms) {
   uint64_t target = reinterpret_cast<uint64_t>(b->mc);
-  if (mode == 2) target = reinterpret_cast<uint64_t>(sym_peer_ptr(b, peer));
+  if (mode == 2 || mode == 5) target = reinterpret_cast<uint64_t>(sym_peer_ptr(b, peer));
   if (mode == 4) target = reinterpret_cast<uint64_t>(b->ptr);
   const size_t n16 = b->bytes / 16;
   cudaEvent_t e0, e1;
