@@ -620,7 +620,7 @@ axonn_status_t agree_all(bool* ok) {
 }
 
 axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
-  if (f.epi.mode == axonn::kRedPair && f.prezeroed) {
+  if ((f.epi.mode == axonn::kRedPair || f.epi.mode == axonn::kMcRed) && f.prezeroed) {
     // zeroed on the copy engines after its last reader; every rank's zeroing
     // is ordered before its barrier, so after it every copy is zero
     f.prezeroed = false;
@@ -636,9 +636,10 @@ axonn_status_t fused_pre(axonn_fc::Fused& f, cudaStream_t st) {
 }
 
 // `buf` (a layer input or output gradient the caller passed) is read for the
-// last time by work already enqueued on `st`.  If it is a kRedPair output of
-// some layer, zero it now on the copy engines, off the critical path; its
-// next fused_pre then only waits for that (AXONN_PREZERO=0: zero inline).
+// last time by work already enqueued on `st`.  If it is the red.add output of
+// some layer (kRedPair or multimem.red), zero it now on the copy engines, off
+// the critical path; its next fused_pre then only waits for that
+// (AXONN_PREZERO=0: zero inline).
 axonn_status_t prezero_after(const void* buf, cudaStream_t st) {
   static const bool on = env_int("AXONN_PREZERO", 1) != 0;
   if (!on || !buf) return AXONN_OK;
@@ -647,7 +648,8 @@ axonn_status_t prezero_after(const void* buf, cudaStream_t st) {
   if (cs != cudaStreamCaptureStatusNone) return AXONN_OK;  // graphs: zero inline at the next use
   for (axonn_fc* o : S.handles) {
     for (axonn_fc::Fused* f : {&o->fo, &o->fi}) {
-      if (f->epi.mode != axonn::kRedPair || f->out.ptr != buf || f->prezeroed) continue;
+      const bool red = f->epi.mode == axonn::kRedPair || f->epi.mode == axonn::kMcRed;
+      if (!red || f->out.ptr != buf || f->prezeroed) continue;
       const size_t bytes = f->elems * f->es;
       if (!S.zstream)
         CUDA_TRY(cudaStreamCreateWithFlags(&S.zstream, cudaStreamNonBlocking));

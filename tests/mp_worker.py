@@ -362,7 +362,7 @@ def main():
                             for a, b in zip(zc, results[(fused, m, k, n, transposed)]):
                                 assert np.array_equal(a, b), f"zero-copy differs {cfg}"
             run_chain(cfg, "uniform", torch.bfloat16, rank)
-            if fused in ("exchange", "redpair"):
+            if fused in ("exchange", "redpair", "red"):
                 run_chain_zero_copy(cfg, rank)
             if fused in ("xsum", "red", "redpair", "exchange", "pairsum", "pairpull", "0"):
                 run_graph(cfg, rank)
