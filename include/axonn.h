@@ -336,6 +336,15 @@ int64_t axonn_kernel_launches(void);
  * are shared by all pairs; a tile's two pieces are summed in fp32 in a fixed
  * order, so results are deterministic).  AXONN_SK=0 turns the split off. */
 int64_t axonn_stream_k_launches(void);
+/* Host-only view of that decomposition: the items CTA pair `pair` of `pairs`
+ * processes, in order, when the first `sk_tiles` tiles (of `num_kb` 64-wide
+ * K-blocks each) are split: tile index, role (0 whole tile, 1 HEAD = K-blocks
+ * [0, h) whose fp32 partial goes to the finisher, 2 TAIL = [t0, num_kb) which
+ * adds the HEAD's partial; at run time a TAIL whose HEAD pair has not started
+ * takes the whole tile instead) and the K-block range [kb0, kb1).  Host
+ * arrays of `cap`; *n = the count (may exceed cap).  Errors: ARG. */
+axonn_status_t axonn_stream_k_items(int sk_tiles, int num_kb, int pair, int pairs, int* tile,
+                                    int* role, int* kb0, int* kb1, int cap, int* n);
 /* SM budget of the persistent GEMM grid (<= 0 or > #SMs: all SMs).  Leaving
  * SMs free lets NCCL kernels run beside the GEMM when collectives overlap. */
 axonn_status_t axonn_set_gemm_sms(int sms);

@@ -112,6 +112,8 @@ _PROTOS = {
     "axonn_profile_read": (_S, [POINTER(c_int64), POINTER(c_double), POINTER(c_double)]),
     "axonn_kernel_launches": (c_int64, []),
     "axonn_stream_k_launches": (c_int64, []),
+    "axonn_stream_k_items": (_S, [c_int, c_int, c_int, c_int, POINTER(c_int), POINTER(c_int),
+                                  POINTER(c_int), POINTER(c_int), c_int, POINTER(c_int)]),
     "axonn_set_gemm_sms": (_S, [c_int]),
     "axonn_comm_bytes": (_S, [POINTER(c_int64), c_int]),
     "axonn_grid_select": (_S, [POINTER(LayerT), c_int, c_int, c_int, POINTER(BwEntry), c_int,
@@ -306,6 +308,16 @@ def axonn_kernel_launches() -> int:
 
 def axonn_stream_k_launches() -> int:
     return _lib.axonn_stream_k_launches()
+
+
+def axonn_stream_k_items(sk_tiles, num_kb, pair, pairs) -> list:
+    """The stream-K items of CTA pair `pair` (host-only; include/axonn.h):
+    a list of (tile, role, kb0, kb1), role 0 whole tile, 1 HEAD, 2 TAIL."""
+    cap = 16
+    arrs = [(c_int * cap)() for _ in range(4)]
+    n = c_int()
+    _check(_lib.axonn_stream_k_items(sk_tiles, num_kb, pair, pairs, *arrs, cap, byref(n)))
+    return [tuple(a[i] for a in arrs) for i in range(min(n.value, cap))]
 
 
 def axonn_set_gemm_sms(sms: int) -> None:

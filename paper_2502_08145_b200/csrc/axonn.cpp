@@ -1505,6 +1505,18 @@ axonn_status_t axonn_profile_read(int64_t* launches, double* ms, double* flops) 
 
 int64_t axonn_kernel_launches(void) { return g_launches.load(); }
 
+axonn_status_t axonn_stream_k_items(int sk_tiles, int num_kb, int pair, int pairs, int* tile,
+                                    int* role, int* kb0, int* kb1, int cap, int* n) {
+  if (sk_tiles < 0 || num_kb < 1 || pairs < 1 || pair < 0 || pair >= pairs || cap < 0 || !n ||
+      (cap > 0 && (!tile || !role || !kb0 || !kb1)))
+    return fail(AXONN_ERR_ARG, "bad argument");
+  // the kernel's decomposition needs every pair's range to span a tile
+  if (static_cast<long long>(sk_tiles) < pairs)
+    return fail(AXONN_ERR_ARG, "stream-K needs sk_tiles >= pairs");
+  *n = axonn::gemm_stream_k_items(sk_tiles, num_kb, pair, pairs, tile, role, kb0, kb1, cap);
+  return AXONN_OK;
+}
+
 int64_t axonn_stream_k_launches(void) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   return axonn::gemm_stream_k_launches();

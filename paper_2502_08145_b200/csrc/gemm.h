@@ -97,6 +97,9 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
 cudaError_t gemm_last_launch_error();
 // launches that used the stream-K tail (axonn_stream_k_launches)
 long long gemm_stream_k_launches();
+// the stream-K items of one CTA pair (axonn_stream_k_items); returns the count
+int gemm_stream_k_items(int sk_tiles, int num_kb, int cluster, int nclusters, int* tile, int* role,
+                        int* kb0, int* kb1, int cap);
 
 // fp32 SIMT FMA (test mode, no TF32): same op codes.
 GemmStatus gemm_f32_simt(int op, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

@@ -317,9 +317,9 @@ struct SkParams {
 
 enum : int { kRoleFull = 0, kRoleHead = 1, kRoleTail = 2, kRoleWhole = 3 };
 
-__device__ __forceinline__ int item_tile(int it) { return it & 0x0FFFFFFF; }
-__device__ __forceinline__ int item_role(int it) { return static_cast<int>(static_cast<unsigned>(it) >> 28); }
-__device__ __forceinline__ int make_item(int tile, int role) { return tile | (role << 28); }
+__host__ __device__ __forceinline__ int item_tile(int it) { return it & 0x0FFFFFFF; }
+__host__ __device__ __forceinline__ int item_role(int it) { return static_cast<int>(static_cast<unsigned>(it) >> 28); }
+__host__ __device__ __forceinline__ int make_item(int tile, int role) { return tile | (role << 28); }
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
@@ -355,7 +355,7 @@ __device__ __forceinline__ uint32_t addf(uint32_t a, float b) {
 
 // the idx-th stream-K item of the pair owning K-block range [u0, u1)
 // (HEAD, whole tiles, TAIL), or -1 past the end
-__device__ __forceinline__ int sk_static_item(int u0, int u1, int kb, int idx) {
+__host__ __device__ __forceinline__ int sk_static_item(int u0, int u1, int kb, int idx) {
   int n = 0;
   if (u1 % kb) {
     if (idx == n) return make_item(u1 / kb, kRoleHead);
@@ -373,7 +373,8 @@ __device__ __forceinline__ int sk_static_item(int u0, int u1, int kb, int idx) {
 }
 
 // K-block range of an item for the pair owning [u0, u1)
-__device__ __forceinline__ void item_kb(int it, int u0, int u1, int kb, int* kb0, int* kb1) {
+__host__ __device__ __forceinline__ void item_kb(int it, int u0, int u1, int kb, int* kb0,
+                                                 int* kb1) {
   const int t = item_tile(it), r = item_role(it);
   *kb0 = r == kRoleTail ? u0 - t * kb : 0;
   *kb1 = r == kRoleHead ? u1 - t * kb : kb;
@@ -1483,5 +1484,28 @@ GemmStatus gemm_bf16_tc(int op, int64_t M, int64_t N, int64_t K, const void* A, 
 cudaError_t gemm_last_launch_error() { return g_launch_error; }
 
 long long gemm_stream_k_launches() { return g_sk_launches; }
+
+// The stream-K items pair `cluster` of `nclusters` processes for a launch
+// whose first sk_tiles tiles (num_kb K-blocks each) are split, in processing
+// order, with the same functions the kernel uses (claims aside: a TAIL whose
+// contributor has not started becomes WHOLE at run time).  Host only.
+int gemm_stream_k_items(int sk_tiles, int num_kb, int cluster, int nclusters, int* tile, int* role,
+                        int* kb0, int* kb1, int cap) {
+  const long long units = static_cast<long long>(sk_tiles) * num_kb;
+  const int u0 = static_cast<int>(units * cluster / nclusters);
+  const int u1 = static_cast<int>(units * (cluster + 1) / nclusters);
+  int n = 0;
+  for (int idx = 0;; ++idx) {
+    const int it = sk_static_item(u0, u1, num_kb, idx);
+    if (it < 0) break;
+    if (n < cap) {
+      tile[n] = item_tile(it);
+      role[n] = item_role(it);
+      item_kb(it, u0, u1, num_kb, &kb0[n], &kb1[n]);
+    }
+    ++n;
+  }
+  return n;
+}
 
 }  // namespace axonn
