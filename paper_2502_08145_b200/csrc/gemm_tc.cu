@@ -10,13 +10,19 @@
 // stages operands with TMA in the layout they already have in HBM — no
 // transposes, no mode tuner.
 //
-// Kernel: persistent, warp-specialised, one CTA per SM.
-//   warp 0      TMA producer   (one elected lane): A/B tiles -> smem ring
-//   warp 1      MMA issuer     (one lane): tcgen05.mma 128x256x16, fp32 in TMEM
-//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//   warps 4..7  epilogue: tcgen05.ld -> RNE bf16 -> global, overlapping the next
-//               tile's main loop (double-buffered accumulator)
-// Tiles: BM=128, BN=256, BK=64 (one 128-byte swizzle row of bf16), 4 stages.
+// Two kernels:
+//   gemm_bf16_tcgen05       1-CTA reference variant (AXONN_GEMM_VARIANT=single):
+//     warp 0 TMA producer, warp 1 MMA issuer (tcgen05.mma 128x256x16), warp 2
+//     TMEM allocator (two 128x256 fp32 accumulators), warps 4..7 epilogue;
+//     BM=128, BN=256, BK=64, 4 stages.
+//   gemm_bf16_tcgen05_pair  the product path (below): CTA pairs
+//     (cta_group::2), 512x256 or 256x256 pair tiles, dynamic tile scheduling,
+//     a stream-K tail for partial waves (SkParams), an 8-warp epilogue that
+//     releases the accumulator as soon as it is in registers (both sub-tiles
+//     first in the 4-stage variant, with setmaxnreg), TMA-store or fused
+//     NVLink epilogues (EpiTarget: red.add pair, multimem.red, exchange,
+//     scatter, ...), an optional memory-bound side task for the idle helper
+//     warps (SideSum), and programmatic dependent launch.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -259,10 +265,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 // halves of B — accumulating into TMEM columns [mt*256, mt*256+256).
 //   MT = 1: 256x256 tile, 5 stages of 32 KiB, two accumulators (the epilogue
 //           of tile i overlaps the main loop of tile i+1);
-//   MT = 2: 512x256 tile, 3 stages of 48 KiB, one accumulator filling all 512
-//           TMEM columns: 33% more flops per byte staged from L2 and a quarter
-//           fewer operand-panel reads per GEMM, which lowers L2/DRAM traffic
-//           and power (the B200 runs power-capped under this load).
+//   MT = 2: 512x256 tile, 4 stages of 48 KiB (DEEP; 3 with AXONN_MT2_DEEP=0),
+//           one accumulator filling all 512 TMEM columns: 33% more flops per
+//           byte staged from L2 and a quarter fewer operand-panel reads per
+//           GEMM, which lowers L2/DRAM traffic and power (the B200 runs
+//           power-capped under this load).
 template <int MT, int DEEP = 0>
 struct PairCfg {
   static constexpr int ROWS_CTA = 128 * MT;
