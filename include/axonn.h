@@ -170,6 +170,15 @@ axonn_status_t axonn_fc_geometry(axonn_fc_t h, axonn_geometry_t* out);
  * buffer that feeds more than one layer needs AXONN_PREZERO=0.
  * Errors: ARG. */
 axonn_status_t axonn_fc_output_buffer(axonn_fc_t h, int which, void** ptr);
+/* The epilogue mode the multi-GPU path picks for a reduction of a rows x cols
+ * output of a GEMM with contraction length kdim over P ranks with
+ * elem_bytes-byte elements (2 bf16, 4 fp32), under the current AXONN_*
+ * switches: "none" (not fused: P = 1, an empty output, rows not a whole number
+ * of 16-B units; NCCL when P > 1), "red_add_pair", "multimem_red",
+ * "exchange", "scatter", "xsum" or "pair_sum" (host buf).  Host only; no
+ * grid needed.  Errors: ARG. */
+axonn_status_t axonn_fused_mode(int P, int elem_bytes, int64_t rows, int64_t cols, int64_t kdim,
+                                char* buf, int cap);
 /* "fused" if collectives along `axis` (0=X,1=Y,2=Z,3=DATA) of the current grid
  * are fused into the GEMM epilogue over NVLS, else the reason (host buf). */
 axonn_status_t axonn_fused_status(int axis, char* buf, int cap);

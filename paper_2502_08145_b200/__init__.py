@@ -97,6 +97,7 @@ _PROTOS = {
     "axonn_fc_prefetch": (_S, [c_void_p, c_void_p, c_void_p]),
     "axonn_fc_output_buffer": (_S, [c_void_p, c_int, POINTER(c_void_p)]),
     "axonn_fused_status": (_S, [c_int, c_char_p, c_int]),
+    "axonn_fused_mode": (_S, [c_int, c_int, c_int64, c_int64, c_int64, c_char_p, c_int]),
     "axonn_nvlink_probe": (_S, [c_int, c_int64, c_int, c_int, c_int, POINTER(c_double)]),
     "axonn_fc_forward": (_S, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "axonn_fc_backward": (_S, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -244,6 +245,13 @@ def axonn_fused_status(axis) -> str:
     a = AXIS[axis] if isinstance(axis, str) else int(axis)
     buf = ctypes.create_string_buffer(256)
     _check(_lib.axonn_fused_status(a, buf, 256))
+    return buf.value.decode()
+
+
+def axonn_fused_mode(P, elem_bytes, rows, cols, kdim) -> str:
+    """The epilogue mode the multi-GPU path picks for this reduction (host only)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.axonn_fused_mode(P, elem_bytes, rows, cols, kdim, buf, 64))
     return buf.value.decode()
 
 

@@ -1122,6 +1122,28 @@ axonn_status_t axonn_nvlink_probe(int axis, int64_t bytes, int mode, int ctas, i
   return AXONN_OK;
 }
 
+axonn_status_t axonn_fused_mode(int P, int elem_bytes, int64_t rows, int64_t cols, int64_t kdim,
+                                char* buf, int cap) {
+  if (P < 1 || (elem_bytes != 2 && elem_bytes != 4) || rows < 0 || cols < 0 || kdim < 0 || !buf ||
+      cap < 1)
+    return fail(AXONN_ERR_ARG, "bad argument");
+  // the same call fused_plan makes, with the same switches
+  const int mode = axonn::fused_mode(P, elem_bytes, rows, cols, kdim,
+                                     env_int("AXONN_RED_MIN_K", 8192),
+                                     env_int("AXONN_EXCHANGE", 1) != 0,
+                                     env_int("AXONN_PAIRSUM", 0) != 0, env_int("AXONN_XSUM", 0),
+                                     env_int("AXONN_REDPAIR", 2));
+  const char* name = mode == axonn::kRedPair    ? "red_add_pair"
+                     : mode == axonn::kMcRed    ? "multimem_red"
+                     : mode == axonn::kExchange ? "exchange"
+                     : mode == axonn::kScatter  ? "scatter"
+                     : mode == axonn::kXSum     ? "xsum"
+                     : mode == axonn::kPairSum  ? "pair_sum"
+                                                : "none";
+  std::snprintf(buf, static_cast<size_t>(cap), "%s", name);
+  return AXONN_OK;
+}
+
 axonn_status_t axonn_fused_status(int axis, char* buf, int cap) {
   if (axis < 0 || axis > 3 || !buf || cap < 1) return fail(AXONN_ERR_ARG, "bad argument");
   const std::string m = S.sym[axis].impl ? std::string("fused") : S.sym_why[axis];
