@@ -50,3 +50,25 @@ def test_block_layers_phases():
     # Table II shapes: QKV h->3h, proj h->h, fc1 h->4h, fc2 4h->h
     assert [(k, n) for _, k, n, _ in a] == [(4096, 12288), (4096, 4096), (4096, 16384), (16384, 4096)]
     assert bench.model_flops(a) == sum(6 * 16384 * k * n for _, k, n, _ in a)
+
+
+def test_measured_table_grid_choice_matches_the_oracle():
+    """bench's grid choice for the data-parallel line and --model runs
+    (model_top1: axonn_grid_select over the measured Case-1 table in
+    profiles/, missing entries at their mean) agrees with oracle.perf_model's
+    ranking over the same table, for the 5B / 20B / 80B blocks at 2, 4, 8 GPUs."""
+    import paper_2502_08145_b200 as ax
+    from oracle import perf_model as pm
+    table, src = bench.case1_table()
+    assert all(v > 0 for v in table.values())
+    for model in ("5B", "20B", "80B"):
+        for world in (2, 4, 8):
+            layers = bench.block_layers(bench.HIDDEN[model], 16384 * world)
+            got, _ = bench.model_top1(ax, layers, world)
+            ref = pm.rank_configs([pm.Layer(*L) for L in layers], world, 8, table, 1.0e11)
+            assert got == tuple(ref[0][0]), (model, world, got, ref[0][0], src)
+            # the C++ ranking's times equal the oracle's on the top entries
+            full = ax.axonn_grid_select(layers, world, 8, table, 1.0e11, 2, 0, cap=5)
+            for c, (cfg, t) in zip(full, ref):
+                assert (c["gx"], c["gy"], c["gz"], c["gd"]) == tuple(cfg)
+                assert abs(c["t_comm"] - t["comm"]) <= 1e-12 * max(1.0, t["comm"])
