@@ -183,7 +183,8 @@ def test_argument_and_state_errors_without_a_device():
 def test_header_is_plain_c_and_links(tmp_path):
     """include/axonn.h is a C ABI: a C99 program compiles against it with
     -Wall -Werror, links to libaxonn.so, and calls pure-host entry points
-    (version, rank <-> coordinates, shard geometry, grid_select) — no torch,
+    (version, rank <-> coordinates, shard geometry, grid_select, the fused
+    reduction mode, the stream-K decomposition) — no torch,
     no C++."""
     import shutil
     import subprocess
@@ -210,6 +211,14 @@ int main(void) {
   if (axonn_shard_geometry(&d, 2, 2, 1, 1, 3, &g) != AXONN_OK) return 4;
   if (axonn_grid_select(&L, 1, 2, 8, &tb, 1, 1e11, 2, 0, out, 4, &n) != AXONN_OK || n != 4) return 5;
   if (axonn_gemm(9, AXONN_BF16, 8, 8, 8, 0, 8, 0, 8, 0, 8, 0) != AXONN_ERR_ARG) return 6;
+  {
+    char mode[32];
+    int tile[4], role[4], k0[4], k1[4], m = 0;
+    if (axonn_fused_mode(2, 2, 8192, 10752, 3584, mode, 32) != AXONN_OK) return 7;
+    if (axonn_stream_k_items(128, 256, 0, 74, tile, role, k0, k1, 4, &m) != AXONN_OK || m < 1)
+      return 8;
+    printf("%s ", mode);
+  }
   printf("ok %d %lld %lld %d%d%d%d\n", axonn_version(), (long long)g.k_l, (long long)g.n_l,
          out[0].gx, out[0].gy, out[0].gz, out[0].gd);
   return 0;
@@ -221,6 +230,8 @@ int main(void) {
                          f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
     assert cc.returncode == 0, cc.stderr
     run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
-    assert run.returncode == 0 and run.stdout.startswith("ok"), (run.returncode, run.stdout, run.stderr)
+    assert run.returncode == 0 and "ok" in run.stdout, (run.returncode, run.stdout, run.stderr)
+    words = run.stdout.split()
+    assert words[0] == "red_add_pair"  # the 2-rank short-K default (axonn_fused_mode)
     # transposed layer on (2,2,1,1): k_l = k/Gx, n_l = n/Gy (R2)
-    assert run.stdout.split()[2:4] == ["512", "256"]
+    assert words[words.index("ok") + 2:words.index("ok") + 4] == ["512", "256"]
