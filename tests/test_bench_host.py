@@ -72,3 +72,21 @@ def test_measured_table_grid_choice_matches_the_oracle():
             for c, (cfg, t) in zip(full, ref):
                 assert (c["gx"], c["gy"], c["gz"], c["gd"]) == tuple(cfg)
                 assert abs(c["t_comm"] - t["comm"]) <= 1e-12 * max(1.0, t["comm"])
+
+
+def test_selection_command_reproduces_the_survey_ranking():
+    """tools/axonn_select.py (the paper's offline configuration selection as a
+    command) on the 80B block, G = 8, Gd = 1, uniform β, phase A: the ranking
+    SURVEY.md §8(c) derives from Eqs. 1-5 (GB per GPU per block: 4x1x2 2.114 <
+    4x2x1 2.416 < 2x2x2 2.517 < 8x1x1 2.819 < 2x1x4 3.121 < 1x2x4 3.926 <
+    2x4x1 4.027 < 1x4x2 4.530 < 1x1x8 6.342 < 1x8x1 8.456)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import axonn_select
+    rows, src = axonn_select.rank("80B", 8, fixed_gd=1, uniform=100.0)
+    got = [(r["gx"], r["gy"], r["gz"]) for r in rows]
+    assert got == [(4, 1, 2), (4, 2, 1), (2, 2, 2), (8, 1, 1), (2, 1, 4), (1, 2, 4), (2, 4, 1),
+                   (1, 4, 2), (1, 1, 8), (1, 8, 1)]
+    # uniform 100 GB/s: t_comm x β = the bytes per GPU of the block
+    want_gb = [2.114, 2.416, 2.517, 2.819, 3.121, 3.926, 4.027, 4.530, 6.342, 8.456]
+    for r, gb in zip(rows, want_gb):
+        assert abs(r["t_comm"] * 100e9 / 1e9 - gb) < 0.0015
